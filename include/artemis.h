@@ -1,0 +1,268 @@
+/*
+ * libartemis — B200 (sm_100a) kernels for the ARTEMIS warp -> octree
+ * rebuild -> render hot path, behind a plain C ABI.
+ *
+ * The reference's native boundary is the flat-array `kernels` module that
+ * animvox/backend.py:19-31 binds (compiled: animvox/_core.pyx, pure:
+ * animvox/_pure.py). Every entry point below replaces one of those
+ * functions, or one of the numpy stages the reference runs around them
+ * (rigging.warp_voxels, rigging.resolve_collisions, volume.build_octree,
+ * geometry.rays_for_camera); the citation is on each declaration.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless a parameter says "host".
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream) and returns an artemis_status for argument errors
+ *    detectable without synchronising. Data-dependent results (counts,
+ *    duplicate detection) are written to device memory the caller reads.
+ *  - Layouts are the reference's: Morton codes u64 with x in the lowest
+ *    interleave slot, 21 bits per axis; tree arrays int32 with leaves encoded
+ *    as ~leaf; FLUT column h*C + c, density last (split here into an fp32
+ *    coefficient block and an fp64 density column).
+ *  - No torch types appear here. The Python layer (paper_2202_05628_b200)
+ *    uses torch only to own device memory and streams.
+ */
+#ifndef ARTEMIS_H
+#define ARTEMIS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *artemis_stream;
+
+typedef enum {
+    ARTEMIS_OK = 0,
+    ARTEMIS_ERR_ARG = 1,        /* null pointer / bad size / unsupported option */
+    ARTEMIS_ERR_RANGE = 2,      /* grid coordinate outside [0, 2^21) (_core.pyx:81-82) */
+    ARTEMIS_ERR_EMPTY = 3,      /* empty leaf set (_core.pyx:196-197) */
+    ARTEMIS_ERR_DUPLICATE = 4,  /* duplicate Morton code (volume.py:244-247) */
+    ARTEMIS_ERR_OOM = 5,
+    ARTEMIS_ERR_CUDA = 6,       /* launch failure; see artemis_last_cuda_error */
+    ARTEMIS_ERR_WORKSPACE = 7,  /* workspace smaller than *_workspace_bytes */
+    ARTEMIS_ERR_NODEVICE = 8    /* no sm_100 device visible */
+} artemis_status;
+
+const char *artemis_version(void);
+const char *artemis_status_string(int status);
+const char *artemis_last_cuda_error(void);
+/* 1 when a CUDA device of compute capability 10.x is visible. */
+int artemis_device_ok(void);
+
+/* ---- Morton codes ------------------------------------------------------
+ * replaces animvox/_core.pyx:79-92 morton_encode, :95-105 morton_decode.
+ * coords: (n, 3) int64 row-major. `range_flag` (device int32, may be NULL)
+ * is set to 1 when any coordinate is outside [0, 2^21) (the caller raises
+ * ValueError, as _core.pyx:81-82 does). */
+int artemis_morton_encode(const int64_t *coords, int64_t n, uint64_t *codes,
+                          int32_t *range_flag, artemis_stream stream);
+int artemis_morton_decode(const uint64_t *codes, int64_t n, int64_t *coords,
+                          artemis_stream stream);
+
+/* ---- Stable radix sort (onesweep, decoupled look-back) --------------------
+ * replaces animvox/_core.pyx:111-167 sort_order (stable LSD, 8-bit digits,
+ * ceil(key_bits/8) passes). Sorts (key, value) pairs ascending by the low
+ * `key_bits` bits of the key; equal keys keep input order. `vals_in` NULL
+ * means values 0..n-1, i.e. the permutation sort_order returns.
+ * n < 2^30. Workspace is caller-allocated device memory. */
+size_t artemis_sort_workspace_bytes(int64_t n, int key_bits, int key_bytes);
+int artemis_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
+                           uint32_t *vals_out, int64_t n, int key_bits, void *workspace,
+                           size_t workspace_bytes, artemis_stream stream);
+int artemis_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                           uint32_t *vals_out, int64_t n, int key_bits, void *workspace,
+                           size_t workspace_bytes, artemis_stream stream);
+
+/* ---- Karras radix tree ------------------------------------------------
+ * replaces animvox/_core.pyx:193-246 build_tree (node numbering, ~leaf child
+ * links and octant boxes identical). codes: strictly sorted u64, n >= 1.
+ * left/right: (n-1) int32, box_min/box_size: (n-1, 3) int32. The root is 0
+ * (n > 1) or ~0 (n == 1), as in the reference. `dup_flag` (device int32,
+ * may be NULL; the caller initialises it to INT32_MAX) receives the
+ * smallest i with codes[i] == codes[i+1] (volume.py:244-247's check). */
+int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *left, int32_t *right,
+                       int32_t *box_min, int32_t *box_size, int32_t *dup_flag,
+                       artemis_stream stream);
+
+/* ---- Traversal structure ------------------------------------------------
+ * The render kernels walk a packed copy of the tree: one 32-byte record per
+ * internal node holding both children's boxes (so a visit is one sector),
+ * plus a super-root record at index max(n-1, 0) whose left child is the
+ * root. Built from the reference arrays (API path) or directly by
+ * artemis_frame_run (device pipeline). nodes: (n) x 32 bytes. */
+int artemis_pack_tree(const uint64_t *codes, int64_t n, int32_t root, const int32_t *left,
+                      const int32_t *right, const int32_t *box_min, const int32_t *box_size,
+                      void *nodes, artemis_stream stream);
+
+/* FLUT (n, width) row-major -> fp32 coefficients (n, width-1) + fp64
+ * density (n). Replaces the FLUT.data gather layout of _core.pyx:536-551. */
+int artemis_flut_split_f64(const double *flut, int64_t n, int width, float *coef,
+                           double *sigma, artemis_stream stream);
+int artemis_flut_split_f32(const float *flut, int64_t n, int width, float *coef,
+                           double *sigma, artemis_stream stream);
+
+typedef struct {
+    const void *nodes;          /* artemis_pack_tree output */
+    const uint32_t *flut_idx;   /* (n_leaves) leaf -> FLUT row */
+    int64_t n_leaves;           /* host value; ignored when n_leaves_dev != NULL */
+    const int32_t *n_leaves_dev;/* device count (device pipeline), may be NULL */
+} artemis_tree_view;
+
+typedef struct {
+    const float *coef;          /* (N, H*C) fp32, column h*C + c */
+    const double *sigma;        /* (N) fp64 density */
+    const int32_t *rot_index;   /* (N) per FLUT row rotation index */
+    const double *rot_inv;      /* (J, 3, 3) fp64 */
+    int degree;                 /* SH degree 0..4 */
+    int channels;               /* C >= 1 */
+    int coef_stride;            /* floats per coef row (FLUT width - 1); 0 = H*C */
+} artemis_shading;
+
+typedef struct {
+    const double *origins_g;    /* (R, 3) grid-space origins */
+    const double *dirs_g;       /* (R, 3) grid-space directions */
+    const double *dirs_w;       /* (R, 3) unit world directions (SH input) */
+    int64_t n_rays;
+    double t_min, t_max;
+} artemis_rays;
+
+/* Pinhole camera, evaluated per pixel exactly as rays_for_camera
+ * (geometry.py:242-263) + _grid_rays (render.py:181-185) do on the host. */
+typedef struct {
+    double R[9];                /* camera-to-world rotation, row-major */
+    double origin[3];           /* camera centre, world */
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double lo[3], cell[3];      /* grid bounds min and cell size */
+} artemis_camera;
+
+/* replaces animvox/_core.pyx:473-559 render_rays. F: (R, C) fp32,
+ * alpha/depth: (R) fp64 (depth +inf when no voxel passed sigma_dep). */
+int artemis_render_rays(const artemis_tree_view *tree, const artemis_shading *shade,
+                        const artemis_rays *rays, double lambda_th, double sigma_dep,
+                        int early_stop, float *F, double *alpha, double *depth,
+                        artemis_stream stream);
+
+/* replaces the count pass of animvox/_core.pyx:586-596 (forward_fit) and
+ * traverse_ray :358-389: hits per ray. counts: (R) int64. */
+int artemis_count_hits(const artemis_tree_view *tree, const artemis_rays *rays, int64_t *counts,
+                       artemis_stream stream);
+
+/* replaces the fill pass of animvox/_core.pyx:597-655 forward_fit: CSR
+ * trace at `offsets` (R+1, exclusive scan of counts) plus F/alpha without
+ * early stop. hit_idx int64, hit_t0/t1 fp64. */
+int artemis_forward_fit(const artemis_tree_view *tree, const artemis_shading *shade,
+                        const artemis_rays *rays, const int64_t *offsets, int64_t *hit_idx,
+                        double *hit_t0, double *hit_t1, float *F, double *alpha,
+                        artemis_stream stream);
+
+/* Device ray generation (parity helper for rays_for_camera + _grid_rays).
+ * og/dg/dw: (W*H, 3) fp64, row-major pixels. */
+int artemis_camera_rays(const artemis_camera *cam /* host */, double *og, double *dg,
+                        double *dw, artemis_stream stream);
+
+/* ---- Warp and collision resolve --------------------------------------
+ * replaces animvox/rigging.py:327-371 (warp_voxels numerics). cells (N,3)
+ * int32 canonical; joint_idx (N,K) int32 (-1 = unused slot); weights (N,K)
+ * fp64; joint_aff (J,12) fp64 = rows 0..2 of the per-joint delta matrices.
+ * lo and cell are HOST pointers to 3 doubles (Bounds.lo, Bounds.cell_size).
+ * Outputs (any may be NULL): positions (N,3) fp64, cells_out (N,3) int32
+ * (-1 when out of bounds), in_bounds (N) uint8, rotation_joint (N) int32. */
+int artemis_warp(const int32_t *cells, int64_t n, int slots, const int32_t *joint_idx,
+                 const double *weights, const double *joint_aff, int n_joints,
+                 const double *lo, const double *cell, int resolution, double *positions,
+                 int32_t *cells_out, uint8_t *in_bounds, int32_t *rotation_joint,
+                 artemis_stream stream);
+
+/* replaces animvox/rigging.py:433-459 (resolve_collisions). Input: the
+ * in-bounds canonical indices' Morton codes sorted STABLY (so equal codes
+ * list canonical indices ascending), n_sorted entries, and the fp64
+ * density per canonical index. Output: live codes (unique, ascending),
+ * winners (highest density, lowest index on ties) and, when pairs != NULL,
+ * the (winner, loser) rows in the reference's (-sigma, index) order.
+ * n_live_out (device int32). Workspace: artemis_resolve_workspace_bytes. */
+size_t artemis_resolve_workspace_bytes(int64_t n_sorted);
+int artemis_resolve_u64(const uint64_t *sorted_codes, const uint32_t *sorted_idx,
+                        int64_t n_sorted, const int32_t *n_sorted_dev, const double *sigma,
+                        uint64_t *live_codes, uint32_t *winners, int64_t *pairs,
+                        int32_t *n_live_out, void *workspace, size_t workspace_bytes,
+                        artemis_stream stream);
+
+/* ---- Device-resident frame pipeline ------------------------------------
+ * One posed frame end to end on the device (render.timed_render_frame,
+ * render.py:284-319): warp -> stable sort of the warped keys -> resolve ->
+ * Karras build -> tile-ordered render with in-kernel ray generation. The
+ * handle owns every intermediate buffer; the asset buffers stay owned by
+ * the caller and must outlive the handle. */
+typedef struct artemis_frame_s *artemis_frame;
+
+typedef struct {
+    int64_t n_voxels;
+    int32_t resolution;         /* power of two <= 2^21 */
+    int32_t slots;              /* K skin-weight slots */
+    int32_t max_joints;
+    int32_t degree, channels;
+    double lo[3], hi[3];
+    const int32_t *cells;       /* (N,3) int32 canonical cells */
+    const int32_t *joint_idx;   /* (N,K) int32 */
+    const double *weights;      /* (N,K) fp64 */
+    const float *coef;          /* (N, H*C) fp32 */
+    const double *sigma;        /* (N) fp64 */
+} artemis_asset;
+
+int artemis_frame_create(const artemis_asset *asset, artemis_frame *out);
+int artemis_frame_destroy(artemis_frame frame);
+
+/* Per-frame inputs are HOST pointers: joint_aff (J,12) fp64 (rows 0..2 of
+ * the per-joint delta matrices, rigging.py:343-345), rot_inv (J,3,3) fp64
+ * (rigging.py:347) and the camera. They are copied into a device parameter
+ * block ahead of the frame, so a captured graph replays unchanged for any
+ * pose and camera of the same image size. joint_aff == NULL renders the
+ * canonical cells (identity warp, render.py:162-167).
+ * flags: bit0 early stop, bit1 capture/replay a CUDA graph (needs a
+ * non-default stream), bit2 also write the reference tree arrays
+ * (left/right/box_min/box_size) for parity checks.
+ * F (W*H, C) fp32, alpha/depth (W*H) fp32, row-major pixels. */
+int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double *rot_inv,
+                      int n_joints, const artemis_camera *cam, double lambda_th,
+                      double sigma_dep, int flags, float *F, float *alpha, float *depth,
+                      artemis_stream stream);
+
+/* Read back the last frame's counts (synchronises the stream). */
+int artemis_frame_counts(artemis_frame frame, int64_t *n_in_bounds, int64_t *n_live,
+                         artemis_stream stream);
+
+/* Device pointers to the last frame's rebuilt tree (reference layout) and
+ * the per-canonical-voxel rotation index, for parity checks. Codes are
+ * 4-byte when 3*log2(resolution)+1 <= 32 (sentinel bit included), else 8. */
+typedef struct {
+    const void *codes;          /* (n_live) Morton codes, code_bytes each */
+    int32_t code_bytes;
+    const uint32_t *flut_idx;   /* (n_live) */
+    const int32_t *left, *right, *box_min, *box_size; /* (n_live-1[,3]), flags bit2 */
+    const int32_t *rotation_joint; /* (N) */
+    const int32_t *n_live_dev;
+    const int32_t *n_in_dev;
+} artemis_frame_tree;
+int artemis_frame_get_tree(artemis_frame frame, artemis_frame_tree *out);
+
+/* Stage timing for eager (non-graph) runs: after artemis_frame_profile(f, 1)
+ * every eager artemis_frame_run records CUDA events between its stages;
+ * artemis_frame_stage_ms writes 5 floats (ms): warp, sort, resolve, build,
+ * render of the last such run (synchronises on its last event). */
+int artemis_frame_profile(artemis_frame frame, int enable);
+int artemis_frame_stage_ms(artemis_frame frame, float *ms);
+
+/* Synchronous device -> host copy (parity helpers). */
+int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);
+
+/* Number of kernel launches one artemis_frame_run enqueues (bench). */
+int artemis_frame_launches(artemis_frame frame);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARTEMIS_H */

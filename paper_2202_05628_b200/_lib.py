@@ -1,0 +1,151 @@
+"""ctypes binding of libartemis.so (the C ABI declared in include/artemis.h).
+
+This is the only place the Python layer touches native code. The library
+is built in-tree by ``build_lib.py``; if it is missing, or no sm_100 device
+is visible, every product call raises ``ExtensionMissing`` -- there is no
+CPU fallback on the product path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import (ContractViolation, DeviceError, DuplicateMortonError, ExtensionMissing)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libartemis.so")
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+INT = C.c_int
+DBL = C.c_double
+SZ = C.c_size_t
+
+OK, ERR_ARG, ERR_RANGE, ERR_EMPTY, ERR_DUP, ERR_OOM, ERR_CUDA, ERR_WS, ERR_NODEV = range(9)
+
+
+class TreeView(C.Structure):
+    _fields_ = [("nodes", P), ("flut_idx", P), ("n_leaves", I64), ("n_leaves_dev", P)]
+
+
+class Shading(C.Structure):
+    _fields_ = [("coef", P), ("sigma", P), ("rot_index", P), ("rot_inv", P), ("degree", INT),
+                ("channels", INT), ("coef_stride", INT)]
+
+
+class Rays(C.Structure):
+    _fields_ = [("origins_g", P), ("dirs_g", P), ("dirs_w", P), ("n_rays", I64),
+                ("t_min", DBL), ("t_max", DBL)]
+
+
+class Camera(C.Structure):
+    _fields_ = [("R", DBL * 9), ("origin", DBL * 3), ("fx", DBL), ("fy", DBL), ("cx", DBL),
+                ("cy", DBL), ("width", I32), ("height", I32), ("lo", DBL * 3),
+                ("cell", DBL * 3)]
+
+
+class Asset(C.Structure):
+    _fields_ = [("n_voxels", I64), ("resolution", I32), ("slots", I32), ("max_joints", I32),
+                ("degree", I32), ("channels", I32), ("lo", DBL * 3), ("hi", DBL * 3),
+                ("cells", P), ("joint_idx", P), ("weights", P), ("coef", P), ("sigma", P)]
+
+
+class FrameTree(C.Structure):
+    _fields_ = [("codes", P), ("code_bytes", I32), ("flut_idx", P), ("left", P), ("right", P),
+                ("box_min", P), ("box_size", P), ("rotation_joint", P), ("n_live_dev", P),
+                ("n_in_dev", P)]
+
+
+_SIGS = {
+    "artemis_version": (C.c_char_p, []),
+    "artemis_status_string": (C.c_char_p, [INT]),
+    "artemis_last_cuda_error": (C.c_char_p, []),
+    "artemis_device_ok": (INT, []),
+    "artemis_morton_encode": (INT, [P, I64, P, P, P]),
+    "artemis_morton_decode": (INT, [P, I64, P, P]),
+    "artemis_sort_workspace_bytes": (SZ, [I64, INT, INT]),
+    "artemis_sort_pairs_u64": (INT, [P, P, P, P, I64, INT, P, SZ, P]),
+    "artemis_sort_pairs_u32": (INT, [P, P, P, P, I64, INT, P, SZ, P]),
+    "artemis_build_tree": (INT, [P, I64, P, P, P, P, P, P]),
+    "artemis_pack_tree": (INT, [P, I64, I32, P, P, P, P, P, P]),
+    "artemis_flut_split_f64": (INT, [P, I64, INT, P, P, P]),
+    "artemis_flut_split_f32": (INT, [P, I64, INT, P, P, P]),
+    "artemis_render_rays": (INT, [C.POINTER(TreeView), C.POINTER(Shading), C.POINTER(Rays), DBL,
+                                  DBL, INT, P, P, P, P]),
+    "artemis_count_hits": (INT, [C.POINTER(TreeView), C.POINTER(Rays), P, P]),
+    "artemis_forward_fit": (INT, [C.POINTER(TreeView), C.POINTER(Shading), C.POINTER(Rays), P, P,
+                                  P, P, P, P, P]),
+    "artemis_camera_rays": (INT, [C.POINTER(Camera), P, P, P, P]),
+    "artemis_warp": (INT, [P, I64, INT, P, P, P, INT, P, P, INT, P, P, P, P, P]),
+    "artemis_resolve_workspace_bytes": (SZ, [I64]),
+    "artemis_resolve_u64": (INT, [P, P, I64, P, P, P, P, P, P, P, SZ, P]),
+    "artemis_frame_create": (INT, [C.POINTER(Asset), C.POINTER(P)]),
+    "artemis_frame_destroy": (INT, [P]),
+    "artemis_frame_run": (INT, [P, P, P, INT, C.POINTER(Camera), DBL, DBL, INT, P, P, P, P]),
+    "artemis_frame_counts": (INT, [P, C.POINTER(I64), C.POINTER(I64), P]),
+    "artemis_frame_get_tree": (INT, [P, C.POINTER(FrameTree)]),
+    "artemis_frame_launches": (INT, [P]),
+    "artemis_copy_to_host": (INT, [P, P, SZ, P]),
+    "artemis_frame_profile": (INT, [P, INT]),
+    "artemis_frame_stage_ms": (INT, [P, C.POINTER(C.c_float)]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """dlopen libartemis.so and declare every exported symbol (no device
+    needed). Raises ExtensionMissing when the file is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ExtensionMissing(
+                f"{path} is not built; run `python -m paper_2202_05628_b200.build_lib`")
+        lib = C.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+_device_checked = False
+
+
+def lib():
+    """The library, after checking an sm_100 device is present."""
+    global _device_checked
+    L = load_library()
+    if not _device_checked:
+        if not L.artemis_device_ok():
+            raise ExtensionMissing("no CUDA device of compute capability 10.x is visible; "
+                                   "the ARTEMIS path has no CPU fallback")
+        _device_checked = True
+    return L
+
+
+def check(status: int, what: str = "") -> None:
+    if status == OK:
+        return
+    L = load_library()
+    msg = L.artemis_status_string(status).decode()
+    if status == ERR_CUDA or status == ERR_OOM:
+        msg += " (" + L.artemis_last_cuda_error().decode() + ")"
+    if status == ERR_RANGE:
+        raise ValueError(f"{what}: {msg}")
+    if status == ERR_EMPTY:
+        raise ValueError(f"{what}: {msg}")
+    if status == ERR_DUP:
+        raise DuplicateMortonError(f"{what}: {msg}")
+    if status == ERR_ARG:
+        raise ContractViolation(f"{what}: {msg}")
+    raise DeviceError(f"{what}: {msg}")

@@ -1,0 +1,107 @@
+// Shared device helpers for libartemis (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "artemis.h"
+
+namespace artemis {
+
+typedef unsigned long long u64;
+
+// ---- status plumbing ------------------------------------------------------
+void set_cuda_error(cudaError_t e);
+int check_launch();  // ARTEMIS_OK or ARTEMIS_ERR_CUDA after a launch
+
+#define ARTEMIS_TRY(expr)                                   \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) {                            \
+            ::artemis::set_cuda_error(_e);                  \
+            return _e == cudaErrorMemoryAllocation ? ARTEMIS_ERR_OOM : ARTEMIS_ERR_CUDA; \
+        }                                                   \
+    } while (0)
+
+#define ARTEMIS_LAUNCHED() ::artemis::check_launch()
+
+inline cudaStream_t S(artemis_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename T>
+inline T ceil_div(T a, T b) { return (a + b - 1) / b; }
+
+// ---- Morton (21 bits per axis, x lowest; animvox/_core.pyx:51-76) ----------
+__host__ __device__ __forceinline__ u64 spread_bits3(u64 v) {
+    v &= 0x1FFFFFull;
+    v = (v | (v << 32)) & 0x1F00000000FFFFull;
+    v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+    v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+    v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+__host__ __device__ __forceinline__ u64 compact_bits3(u64 v) {
+    v &= 0x1249249249249249ull;
+    v = (v ^ (v >> 2)) & 0x10C30C30C30C30C3ull;
+    v = (v ^ (v >> 4)) & 0x100F00F00F00F00Full;
+    v = (v ^ (v >> 8)) & 0x1F0000FF0000FFull;
+    v = (v ^ (v >> 16)) & 0x1F00000000FFFFull;
+    v = (v ^ (v >> 32)) & 0x1FFFFFull;
+    return v;
+}
+
+__host__ __device__ __forceinline__ u64 morton3(u64 x, u64 y, u64 z) {
+    return spread_bits3(x) | (spread_bits3(y) << 1) | (spread_bits3(z) << 2);
+}
+
+// ---- packed traversal node --------------------------------------------------
+// One internal node = 32 bytes: both children's octant boxes (min corner
+// plus the number of free Morton bits, which fixes the per-axis power-of-two
+// size exactly as _core.pyx:182-190 does) and the child links.
+// word[0] = L.x | L.free << 21, word[1] = L.y, word[2] = L.z, word[3] = left
+// word[4] = R.x | R.free << 21, word[5] = R.y, word[6] = R.z, word[7] = right
+// A child with free == kAbsent does not exist (the super-root's right).
+constexpr uint32_t kAbsent = 0x7FF;
+
+struct PackedNode {
+    uint32_t w[8];
+};
+
+__host__ __device__ __forceinline__ int box_size_axis(int free_bits, int axis) {
+    return 1 << ((free_bits + 2 - axis) / 3);
+}
+
+// number of differing low bits between the first and last code of a range
+__device__ __forceinline__ int range_free_bits(u64 a, u64 b) {
+    return a == b ? 0 : 64 - __clzll(static_cast<long long>(a ^ b));
+}
+
+__device__ __forceinline__ void pack_child(uint32_t *w, u64 c_first, u64 c_last, int link) {
+    int fb = range_free_bits(c_first, c_last);
+    u64 base = fb >= 64 ? 0ull : (c_first >> fb) << fb;
+    w[0] = static_cast<uint32_t>(compact_bits3(base)) | (static_cast<uint32_t>(fb) << 21);
+    w[1] = static_cast<uint32_t>(compact_bits3(base >> 1));
+    w[2] = static_cast<uint32_t>(compact_bits3(base >> 2));
+    w[3] = static_cast<uint32_t>(link);
+}
+
+// ---- warp helpers -----------------------------------------------------------
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+}  // namespace artemis

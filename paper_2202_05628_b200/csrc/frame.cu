@@ -1,0 +1,320 @@
+// Device-resident frame pipeline: warp -> stable sort -> resolve -> Karras
+// build -> render, enqueued as one stream-ordered sequence and (optionally)
+// captured once into a CUDA graph that every later frame replays.
+//
+// Replaces one call of animvox/render.py:284-319 (timed_render_frame):
+//   warp_voxels          rigging.py:327-397    -> lbs_warp_kernel (keys, rotation joint)
+//   resolve_collisions   rigging.py:419-459    -> onesweep sort + resolve kernels
+//   build_octree         volume.py:212-261     -> build_tree_kernel (+ packed nodes)
+//   render_view          render.py:322-363     -> render_kernel, camera rays in-kernel
+// The in-bounds and live counts never leave the device: every kernel after
+// the warp sizes its grid for the worst case and reads the count.
+// Per-frame inputs (joint deltas, inverse rotations, camera) are copied into
+// a device parameter block before the graph launch, so the graph itself is
+// pose- and camera-independent.
+#include <string.h>
+
+#include "common.cuh"
+#include "tree.cuh"
+
+namespace artemis {
+
+int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jidx,
+                  const double *w, const double *aff, int n_joints, const double lo[3],
+                  const double cell[3], int res, int key_bytes, void *keys, uint32_t *vals,
+                  int32_t *rot_joint, int32_t *n_in, uint64_t sentinel, int identity,
+                  cudaStream_t st);
+int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
+                  const artemis_camera *cam_dev, int width, int height, double lambda_th,
+                  double sigma_dep, int early_stop, float *F, float *A, float *D,
+                  cudaStream_t st);
+
+constexpr int kMaxFrameJoints = 256;
+
+struct FrameParams {
+    artemis_camera cam;
+    double aff[kMaxFrameJoints * 12];
+    double rot_inv[kMaxFrameJoints * 9];
+};
+
+}  // namespace artemis
+
+using namespace artemis;
+
+struct artemis_frame_s {
+    artemis_asset asset;
+    int64_t n;
+    int key_bytes, key_bits;
+    uint64_t sentinel;
+    double lo[3], cell[3];
+    void *keys = nullptr, *keys_sorted = nullptr, *live_codes = nullptr;
+    uint32_t *vals = nullptr, *vals_sorted = nullptr, *winners = nullptr;
+    int32_t *rot_joint = nullptr, *counters = nullptr;
+    int32_t *left = nullptr, *right = nullptr, *bmin = nullptr, *bsize = nullptr;
+    PackedNode *nodes = nullptr;
+    void *sort_ws = nullptr, *resolve_ws = nullptr;
+    size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
+    FrameParams *params = nullptr;
+    // captured graph and the launch shape it was captured for
+    cudaGraphExec_t exec = nullptr;
+    int g_w = 0, g_h = 0, g_flags = 0, g_identity = -1, g_nj = 0;
+    const void *g_F = nullptr, *g_A = nullptr, *g_D = nullptr;
+    cudaStream_t g_stream = nullptr;
+    double g_lambda = 0, g_sigma_dep = 0;
+    int launches = 0;
+    // stage profiling (eager runs only): events before warp, sort, resolve,
+    // build, render and after render
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int profile = 0;
+};
+
+namespace {
+
+template <typename T>
+int dev_alloc(T **p, size_t bytes) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        set_cuda_error(e);
+        return ARTEMIS_ERR_OOM;
+    }
+    return ARTEMIS_OK;
+}
+
+int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int height,
+                  double lambda_th, double sigma_dep, int flags, float *F, float *A, float *D,
+                  cudaStream_t st) {
+    const artemis_asset &as = f->asset;
+    int rc;
+    int launches = 0;
+    const bool prof = f->profile && !(flags & 2);
+    auto mark = [&](int k) {
+        if (prof) cudaEventRecord(f->ev[k], st);
+    };
+    mark(0);
+    ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 2 * sizeof(int32_t), st));
+    rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,
+                       identity ? 1 : n_joints, f->lo, f->cell, as.resolution, f->key_bytes,
+                       f->keys, f->vals, f->rot_joint, f->counters, f->sentinel, identity, st);
+    if (rc) return rc;
+    launches += 1;
+    mark(1);
+    const bool write_ref = (flags & 4) != 0;
+    if (f->key_bytes == 4) {
+        rc = sort_pairs<uint32_t>((const uint32_t *)f->keys, f->vals, (uint32_t *)f->keys_sorted,
+                                  f->vals_sorted, f->n, f->key_bits, f->sort_ws, f->sort_ws_bytes,
+                                  st);
+        if (rc) return rc;
+        mark(2);
+        rc = resolve<uint32_t>((const uint32_t *)f->keys_sorted, f->vals_sorted, f->n,
+                               f->counters, as.sigma, (uint32_t *)f->live_codes, f->winners,
+                               nullptr, f->counters + 1, f->resolve_ws, f->resolve_ws_bytes, st);
+        if (rc) return rc;
+        mark(3);
+        rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
+                                         f->n, write_ref ? f->left : nullptr, f->right, f->bmin,
+                                         f->bsize, f->nodes, nullptr, st);
+    } else {
+        rc = sort_pairs<u64>((const u64 *)f->keys, f->vals, (u64 *)f->keys_sorted, f->vals_sorted,
+                             f->n, f->key_bits, f->sort_ws, f->sort_ws_bytes, st);
+        if (rc) return rc;
+        mark(2);
+        rc = resolve<u64>((const u64 *)f->keys_sorted, f->vals_sorted, f->n, f->counters,
+                          as.sigma, (u64 *)f->live_codes, f->winners, nullptr, f->counters + 1,
+                          f->resolve_ws, f->resolve_ws_bytes, st);
+        if (rc) return rc;
+        mark(3);
+        rc = launch_build_tree<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n,
+                                    write_ref ? f->left : nullptr, f->right, f->bmin, f->bsize,
+                                    f->nodes, nullptr, st);
+    }
+    if (rc) return rc;
+    mark(4);
+    const int passes = f->key_bits <= 0 ? 1 : (f->key_bits + 7) / 8;
+    launches += 2 + passes + 3 + 1;
+    artemis_tree_view tv{f->nodes, f->winners, 0, f->counters + 1};
+    artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
+                       as.channels, 0};
+    rc = render_camera(&tv, &sh, &f->params->cam, width, height, lambda_th, sigma_dep,
+                       flags & 1, F, A, D, st);
+    mark(5);
+    launches += 1;
+    f->launches = launches;
+    return rc;
+}
+
+}  // namespace
+
+extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) {
+    if (!a || !out || a->n_voxels < 1 || a->n_voxels >= (int64_t(1) << 30) || a->slots < 1 ||
+        a->max_joints < 1 || a->max_joints > kMaxFrameJoints || a->degree < 0 || a->degree > 4 ||
+        a->channels < 1 || a->resolution < 1 || (a->resolution & (a->resolution - 1)) ||
+        a->resolution > (1 << 21) || !a->cells || !a->joint_idx || !a->weights || !a->coef ||
+        !a->sigma)
+        return ARTEMIS_ERR_ARG;
+    artemis_frame f = new artemis_frame_s();
+    f->asset = *a;
+    f->n = a->n_voxels;
+    int levels = 0;
+    while ((1 << levels) < a->resolution) ++levels;
+    f->key_bits = 3 * levels + 1;  // one extra bit for the out-of-bounds sentinel
+    f->key_bytes = f->key_bits <= 32 ? 4 : 8;
+    f->sentinel = uint64_t(1) << (3 * levels);
+    for (int k = 0; k < 3; ++k) {
+        f->lo[k] = a->lo[k];
+        f->cell[k] = (a->hi[k] - a->lo[k]) / a->resolution;  // Bounds.cell_size (volume.py:45-46)
+    }
+    const int64_t n = f->n;
+    int rc = ARTEMIS_OK;
+    rc = rc ? rc : dev_alloc(&f->keys, n * f->key_bytes);
+    rc = rc ? rc : dev_alloc(&f->keys_sorted, n * f->key_bytes);
+    rc = rc ? rc : dev_alloc(&f->live_codes, n * f->key_bytes);
+    rc = rc ? rc : dev_alloc(&f->vals, n * 4);
+    rc = rc ? rc : dev_alloc(&f->vals_sorted, n * 4);
+    rc = rc ? rc : dev_alloc(&f->winners, n * 4);
+    rc = rc ? rc : dev_alloc(&f->rot_joint, n * 4);
+    rc = rc ? rc : dev_alloc(&f->counters, 64);
+    rc = rc ? rc : dev_alloc(&f->left, n * 4);
+    rc = rc ? rc : dev_alloc(&f->right, n * 4);
+    rc = rc ? rc : dev_alloc(&f->bmin, n * 12);
+    rc = rc ? rc : dev_alloc(&f->bsize, n * 12);
+    rc = rc ? rc : dev_alloc(&f->nodes, (n + 1) * sizeof(PackedNode));
+    f->sort_ws_bytes = sort_workspace_bytes(n, f->key_bits, f->key_bytes);
+    f->resolve_ws_bytes = resolve_workspace_bytes(n);
+    rc = rc ? rc : dev_alloc(&f->sort_ws, f->sort_ws_bytes);
+    rc = rc ? rc : dev_alloc(&f->resolve_ws, f->resolve_ws_bytes);
+    rc = rc ? rc : dev_alloc(&f->params, sizeof(FrameParams));
+    if (rc) {
+        artemis_frame_destroy(f);
+        return rc;
+    }
+    *out = f;
+    return ARTEMIS_OK;
+}
+
+extern "C" int artemis_frame_destroy(artemis_frame f) {
+    if (!f) return ARTEMIS_OK;
+    if (f->exec) cudaGraphExecDestroy(f->exec);
+    for (cudaEvent_t e : f->ev)
+        if (e) cudaEventDestroy(e);
+    void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
+                    f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
+                    f->sort_ws, f->resolve_ws, f->params};
+    for (void *b : bufs)
+        if (b) cudaFree(b);
+    delete f;
+    return ARTEMIS_OK;
+}
+
+extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const double *rot_inv,
+                                 int n_joints, const artemis_camera *cam, double lambda_th,
+                                 double sigma_dep, int flags, float *F, float *alpha,
+                                 float *depth, artemis_stream stream) {
+    if (!f || !cam || !F || !alpha || !depth || cam->width < 1 || cam->height < 1)
+        return ARTEMIS_ERR_ARG;
+    const int identity = joint_aff == nullptr;
+    if (!identity && (!rot_inv || n_joints < 1 || n_joints > f->asset.max_joints))
+        return ARTEMIS_ERR_ARG;
+    cudaStream_t st = S(stream);
+    // parameter block: camera + joint tables (host -> device, before the graph)
+    ARTEMIS_TRY(cudaMemcpyAsync(&f->params->cam, cam, sizeof(artemis_camera),
+                                cudaMemcpyHostToDevice, st));
+    if (identity) {
+        static const double eye[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, eye, sizeof(eye), cudaMemcpyHostToDevice, st));
+    } else {
+        ARTEMIS_TRY(cudaMemcpyAsync(f->params->aff, joint_aff, sizeof(double) * 12 * n_joints,
+                                    cudaMemcpyHostToDevice, st));
+        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, rot_inv, sizeof(double) * 9 * n_joints,
+                                    cudaMemcpyHostToDevice, st));
+    }
+    const int use_graph = (flags & 2) && st != nullptr;
+    if (!use_graph)
+        return enqueue_frame(f, identity, n_joints, cam->width, cam->height, lambda_th, sigma_dep,
+                             flags, F, alpha, depth, st);
+    const bool same = f->exec && f->g_w == cam->width && f->g_h == cam->height &&
+                      f->g_flags == flags && f->g_identity == identity && f->g_nj == n_joints &&
+                      f->g_F == F && f->g_A == alpha && f->g_D == depth && f->g_stream == st &&
+                      f->g_lambda == lambda_th && f->g_sigma_dep == sigma_dep;
+    if (!same) {
+        if (f->exec) {
+            cudaGraphExecDestroy(f->exec);
+            f->exec = nullptr;
+        }
+        ARTEMIS_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, lambda_th,
+                               sigma_dep, flags, F, alpha, depth, st);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) {
+            set_cuda_error(e);
+            return ARTEMIS_ERR_CUDA;
+        }
+        e = cudaGraphInstantiate(&f->exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            set_cuda_error(e);
+            f->exec = nullptr;
+            return ARTEMIS_ERR_CUDA;
+        }
+        f->g_w = cam->width;
+        f->g_h = cam->height;
+        f->g_flags = flags;
+        f->g_identity = identity;
+        f->g_nj = n_joints;
+        f->g_F = F;
+        f->g_A = alpha;
+        f->g_D = depth;
+        f->g_stream = st;
+        f->g_lambda = lambda_th;
+        f->g_sigma_dep = sigma_dep;
+    }
+    ARTEMIS_TRY(cudaGraphLaunch(f->exec, st));
+    return ARTEMIS_OK;
+}
+
+extern "C" int artemis_frame_counts(artemis_frame f, int64_t *n_in, int64_t *n_live,
+                                    artemis_stream stream) {
+    if (!f) return ARTEMIS_ERR_ARG;
+    int32_t h[2] = {0, 0};
+    ARTEMIS_TRY(cudaMemcpyAsync(h, f->counters, sizeof(h), cudaMemcpyDeviceToHost, S(stream)));
+    ARTEMIS_TRY(cudaStreamSynchronize(S(stream)));
+    if (n_in) *n_in = h[0];
+    if (n_live) *n_live = h[1];
+    return ARTEMIS_OK;
+}
+
+extern "C" int artemis_frame_get_tree(artemis_frame f, artemis_frame_tree *out) {
+    if (!f || !out) return ARTEMIS_ERR_ARG;
+    out->codes = f->live_codes;
+    out->code_bytes = f->key_bytes;
+    out->flut_idx = f->winners;
+    out->left = f->left;
+    out->right = f->right;
+    out->box_min = f->bmin;
+    out->box_size = f->bsize;
+    out->rotation_joint = f->rot_joint;
+    out->n_live_dev = f->counters + 1;
+    out->n_in_dev = f->counters;
+    return ARTEMIS_OK;
+}
+
+extern "C" int artemis_frame_launches(artemis_frame f) { return f ? f->launches : 0; }
+
+extern "C" int artemis_frame_profile(artemis_frame f, int enable) {
+    if (!f) return ARTEMIS_ERR_ARG;
+    if (enable && !f->ev[0])
+        for (auto &e : f->ev) ARTEMIS_TRY(cudaEventCreate(&e));
+    f->profile = enable ? 1 : 0;
+    return ARTEMIS_OK;
+}
+
+extern "C" int artemis_frame_stage_ms(artemis_frame f, float *ms) {
+    if (!f || !ms || !f->ev[0]) return ARTEMIS_ERR_ARG;
+    ARTEMIS_TRY(cudaEventSynchronize(f->ev[5]));
+    for (int k = 0; k < 5; ++k) ARTEMIS_TRY(cudaEventElapsedTime(ms + k, f->ev[k], f->ev[k + 1]));
+    return ARTEMIS_OK;
+}

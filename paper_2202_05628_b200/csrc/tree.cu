@@ -1,0 +1,218 @@
+// Morton codes, Karras radix-tree build and the packed traversal layout.
+//
+// build_tree follows animvox/_core.pyx:193-246 node for node: direction from
+// the neighbouring prefix lengths, exponential then binary range search,
+// split bisection, ~leaf child links, octant boxes from the common prefix.
+// One thread per internal node; the same thread also writes the node's
+// 32-byte packed record (both children's boxes) for the render kernels, so
+// the device pipeline never re-derives boxes at traversal time.
+#include "common.cuh"
+#include "tree.cuh"
+
+namespace artemis {
+
+__global__ void morton_encode_kernel(const int64_t *__restrict__ xyz, int64_t n,
+                                     u64 *__restrict__ codes, int32_t *__restrict__ range_flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    const int64_t lim = int64_t(1) << 21;
+    if (range_flag && (x < 0 || y < 0 || z < 0 || x >= lim || y >= lim || z >= lim))
+        *range_flag = 1;
+    codes[i] = morton3((u64)x, (u64)y, (u64)z);
+}
+
+__global__ void morton_decode_kernel(const u64 *__restrict__ codes, int64_t n,
+                                     int64_t *__restrict__ xyz) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    u64 c = codes[i];
+    xyz[3 * i] = (int64_t)compact_bits3(c);
+    xyz[3 * i + 1] = (int64_t)compact_bits3(c >> 1);
+    xyz[3 * i + 2] = (int64_t)compact_bits3(c >> 2);
+}
+
+template <typename K>
+__device__ __forceinline__ int prefix_len(const K *__restrict__ c, int64_t n, int64_t i,
+                                          int64_t j) {
+    if (j < 0 || j >= n) return -1;
+    u64 x = (u64)c[i] ^ (u64)c[j];
+    return x ? __clzll((long long)x) : 64;
+}
+
+// Karras node i (i < n-1). Writes reference arrays (when non-null) and the
+// packed record; node 0 also writes the super-root record at index n-1.
+template <typename K>
+__device__ void build_node(const K *__restrict__ c, int64_t n, int64_t i, int32_t *left,
+                           int32_t *right, int32_t *bmin, int32_t *bsize, PackedNode *nodes,
+                           int32_t *dup_flag) {
+    int dir = prefix_len(c, n, i, i + 1) > prefix_len(c, n, i, i - 1) ? 1 : -1;
+    int floor_len = prefix_len(c, n, i, i - dir);
+    int64_t hi = 2;
+    while (prefix_len(c, n, i, i + hi * dir) > floor_len) hi <<= 1;
+    int64_t len = 0;
+    for (int64_t t = hi >> 1; t >= 1; t >>= 1)
+        if (prefix_len(c, n, i, i + (len + t) * dir) > floor_len) len += t;
+    int64_t j = i + len * dir;
+    int64_t first = dir > 0 ? i : j, last = dir > 0 ? j : i;
+    int node_len = prefix_len(c, n, first, last);
+    int64_t split = first, step = last - first;
+    do {
+        step = (step + 1) >> 1;
+        if (split + step < last && prefix_len(c, n, first, split + step) > node_len)
+            split += step;
+    } while (step > 1);
+    int32_t l = split == first ? ~(int32_t)split : (int32_t)split;
+    int32_t r = split + 1 == last ? ~(int32_t)(split + 1) : (int32_t)(split + 1);
+    u64 cf = (u64)c[first], cl = (u64)c[last];
+    if (left) {
+        left[i] = l;
+        right[i] = r;
+        int fb = range_free_bits(cf, cl);
+        u64 base = fb >= 64 ? 0ull : (cf >> fb) << fb;
+        bmin[3 * i] = (int32_t)compact_bits3(base);
+        bmin[3 * i + 1] = (int32_t)compact_bits3(base >> 1);
+        bmin[3 * i + 2] = (int32_t)compact_bits3(base >> 2);
+        bsize[3 * i] = box_size_axis(fb, 0);
+        bsize[3 * i + 1] = box_size_axis(fb, 1);
+        bsize[3 * i + 2] = box_size_axis(fb, 2);
+    }
+    if (nodes) {
+        PackedNode p;
+        pack_child(p.w, cf, (u64)c[split], l);
+        pack_child(p.w + 4, (u64)c[split + 1], cl, r);
+        reinterpret_cast<uint4 *>(nodes + i)[0] = make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]);
+        reinterpret_cast<uint4 *>(nodes + i)[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
+        if (i == 0) {
+            PackedNode s;
+            pack_child(s.w, (u64)c[0], (u64)c[n - 1], 0);
+            s.w[4] = kAbsent << 21;
+            s.w[5] = s.w[6] = 0;
+            s.w[7] = 0;
+            reinterpret_cast<uint4 *>(nodes + (n - 1))[0] = make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
+            reinterpret_cast<uint4 *>(nodes + (n - 1))[1] = make_uint4(s.w[4], s.w[5], s.w[6], s.w[7]);
+        }
+    }
+    if (dup_flag && c[i] == c[i + 1]) atomicMin(dup_flag, (int32_t)i);
+}
+
+template <typename K>
+__global__ void build_tree_kernel(const K *__restrict__ codes, int64_t n_host,
+                                  const int32_t *__restrict__ n_dev, int32_t *left, int32_t *right,
+                                  int32_t *bmin, int32_t *bsize, PackedNode *nodes,
+                                  int32_t *dup_flag) {
+    int64_t n = n_dev ? (int64_t)*n_dev : n_host;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n == 1 && i == 0 && nodes) {
+        // single leaf: root = ~0, only the super-root record exists
+        PackedNode s;
+        u64 c0 = (u64)codes[0];
+        pack_child(s.w, c0, c0, ~0);
+        s.w[4] = kAbsent << 21;
+        s.w[5] = s.w[6] = s.w[7] = 0;
+        reinterpret_cast<uint4 *>(nodes)[0] = make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
+        reinterpret_cast<uint4 *>(nodes)[1] = make_uint4(s.w[4], s.w[5], s.w[6], s.w[7]);
+        return;
+    }
+    if (i >= n - 1) return;
+    build_node(codes, n, i, left, right, bmin, bsize, nodes, dup_flag);
+}
+
+// API path: packed records from the reference arrays (any valid tree).
+__global__ void pack_tree_kernel(const u64 *__restrict__ codes, int64_t n, int32_t root,
+                                 const int32_t *__restrict__ left, const int32_t *__restrict__ right,
+                                 const int32_t *__restrict__ bmin,
+                                 const int32_t *__restrict__ bsize, PackedNode *nodes) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    auto child = [&](uint32_t *w, int32_t link) {
+        if (link < 0) {
+            u64 c = codes[~link];
+            w[0] = (uint32_t)compact_bits3(c);
+            w[1] = (uint32_t)compact_bits3(c >> 1);
+            w[2] = (uint32_t)compact_bits3(c >> 2);
+        } else {
+            const int32_t *m = bmin + 3 * link, *s = bsize + 3 * link;
+            int fb = (__ffs(s[0]) - 1) + (__ffs(s[1]) - 1) + (__ffs(s[2]) - 1);
+            w[0] = (uint32_t)m[0] | ((uint32_t)fb << 21);
+            w[1] = (uint32_t)m[1];
+            w[2] = (uint32_t)m[2];
+        }
+        w[3] = (uint32_t)link;
+    };
+    PackedNode p;
+    if (i < n - 1) {
+        child(p.w, left[i]);
+        child(p.w + 4, right[i]);
+    } else if (i == (n > 1 ? n - 1 : 0)) {
+        child(p.w, root);
+        p.w[4] = kAbsent << 21;
+        p.w[5] = p.w[6] = p.w[7] = 0;
+    } else {
+        return;
+    }
+    reinterpret_cast<uint4 *>(nodes + i)[0] = make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]);
+    reinterpret_cast<uint4 *>(nodes + i)[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
+}
+
+template <typename K>
+int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
+                      int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
+                      PackedNode *nodes, int32_t *dup_flag, cudaStream_t st) {
+    int64_t threads = n_cap > 1 ? n_cap - 1 : 1;
+    int blocks = (int)ceil_div<int64_t>(threads, 256);
+    build_tree_kernel<K><<<blocks, 256, 0, st>>>(codes, n_host, n_dev, left, right, bmin, bsize,
+                                                  nodes, dup_flag);
+    return ARTEMIS_LAUNCHED();
+}
+
+template int launch_build_tree<u64>(const u64 *, int64_t, const int32_t *, int64_t, int32_t *,
+                                    int32_t *, int32_t *, int32_t *, PackedNode *, int32_t *,
+                                    cudaStream_t);
+template int launch_build_tree<uint32_t>(const uint32_t *, int64_t, const int32_t *, int64_t,
+                                         int32_t *, int32_t *, int32_t *, int32_t *,
+                                         PackedNode *, int32_t *, cudaStream_t);
+
+}  // namespace artemis
+
+using namespace artemis;
+
+extern "C" int artemis_morton_encode(const int64_t *coords, int64_t n, uint64_t *codes,
+                                     int32_t *range_flag, artemis_stream stream) {
+    if (n < 0 || (n > 0 && (!coords || !codes))) return ARTEMIS_ERR_ARG;
+    if (n == 0) return ARTEMIS_OK;
+    morton_encode_kernel<<<(int)ceil_div<int64_t>(n, 256), 256, 0, S(stream)>>>(
+        coords, n, reinterpret_cast<u64 *>(codes), range_flag);
+    return ARTEMIS_LAUNCHED();
+}
+
+extern "C" int artemis_morton_decode(const uint64_t *codes, int64_t n, int64_t *coords,
+                                     artemis_stream stream) {
+    if (n < 0 || (n > 0 && (!coords || !codes))) return ARTEMIS_ERR_ARG;
+    if (n == 0) return ARTEMIS_OK;
+    morton_decode_kernel<<<(int)ceil_div<int64_t>(n, 256), 256, 0, S(stream)>>>(
+        reinterpret_cast<const u64 *>(codes), n, coords);
+    return ARTEMIS_LAUNCHED();
+}
+
+extern "C" int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *left, int32_t *right,
+                                  int32_t *box_min, int32_t *box_size, int32_t *dup_flag,
+                                  artemis_stream stream) {
+    if (n < 0 || !codes) return ARTEMIS_ERR_ARG;
+    if (n == 0) return ARTEMIS_ERR_EMPTY;
+    if (n == 1) return ARTEMIS_OK;
+    if (!left || !right || !box_min || !box_size) return ARTEMIS_ERR_ARG;
+    return launch_build_tree<u64>(reinterpret_cast<const u64 *>(codes), n, nullptr, n, left,
+                                  right, box_min, box_size, nullptr, dup_flag, S(stream));
+}
+
+extern "C" int artemis_pack_tree(const uint64_t *codes, int64_t n, int32_t root,
+                                 const int32_t *left, const int32_t *right,
+                                 const int32_t *box_min, const int32_t *box_size, void *nodes,
+                                 artemis_stream stream) {
+    if (n < 1 || !codes || !nodes) return ARTEMIS_ERR_ARG;
+    if (n > 1 && (!left || !right || !box_min || !box_size)) return ARTEMIS_ERR_ARG;
+    pack_tree_kernel<<<(int)ceil_div<int64_t>(n, 256), 256, 0, S(stream)>>>(
+        reinterpret_cast<const u64 *>(codes), n, root, left, right, box_min, box_size,
+        reinterpret_cast<PackedNode *>(nodes));
+    return ARTEMIS_LAUNCHED();
+}

@@ -1,0 +1,195 @@
+"""Device-resident frame pipeline (the throughput path).
+
+One ``FramePipeline`` holds a character on the device -- canonical cells,
+skin weights, the FLUT split into fp32 SH coefficients and fp64 density --
+and renders posed frames with ``artemis_frame_run``: warp -> stable onesweep
+sort -> collision resolve -> Karras build -> tile-ordered render with
+in-kernel camera rays, all stream-ordered, the in-bounds / live counts
+never leaving the device, and the whole sequence captured once as a CUDA
+graph and replayed for every later pose/camera of the same image size.
+
+Host work per frame is what the reference also does on the host: forward
+kinematics over J joints (kinematics.pose_tables, rigging.py:228-247,
+343-347) and the camera set-up.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from . import kinematics as KM
+from ._lib import check
+from .device import download, empty, ptr, upload
+
+
+class FramePipeline:
+    def __init__(self, cells, skin_idx, skin_w, flut, degree: int, channels: int,
+                 resolution: int, lo, hi, rig: KM.Rig | None = None, max_joints: int | None = None,
+                 stream: torch.cuda.Stream | None = None):
+        L = _lib.lib()
+        self.stream = stream or torch.cuda.Stream()
+        cells = np.ascontiguousarray(cells, dtype=np.int32)
+        self.n = int(cells.shape[0])
+        self.degree, self.channels = int(degree), int(channels)
+        self.resolution = int(resolution)
+        self.lo = np.asarray(lo, dtype=np.float64)
+        self.hi = np.asarray(hi, dtype=np.float64)
+        self.cell = (self.hi - self.lo) / self.resolution
+        self.rig = rig
+        self._canon = KM.canonical_globals(rig) if rig is not None else None
+        with torch.cuda.stream(self.stream):
+            self.d_cells = upload(cells, np.int32)
+            self.d_jidx = upload(np.ascontiguousarray(skin_idx, dtype=np.int32), np.int32)
+            self.d_w = upload(np.ascontiguousarray(skin_w, dtype=np.float64), np.float64)
+            fl = np.asarray(flut)
+            width = fl.shape[1]
+            self.coef = empty((self.n, width - 1), np.float32)
+            self.sigma = empty(self.n, np.float64)
+            sh = self.stream.cuda_stream or None
+            if fl.dtype == np.float32:
+                d_fl = upload(fl, np.float32)
+                check(L.artemis_flut_split_f32(ptr(d_fl), self.n, width, ptr(self.coef),
+                                               ptr(self.sigma), sh), "flut_split")
+            else:
+                d_fl = upload(fl, np.float64)
+                check(L.artemis_flut_split_f64(ptr(d_fl), self.n, width, ptr(self.coef),
+                                               ptr(self.sigma), sh), "flut_split")
+            self.stream.synchronize()
+            del d_fl
+        a = _lib.Asset()
+        a.n_voxels = self.n
+        a.resolution = self.resolution
+        a.slots = int(self.d_jidx.shape[1])
+        a.max_joints = int(max_joints or (rig.n_joints if rig is not None else 1))
+        a.degree, a.channels = self.degree, self.channels
+        a.lo[:] = [float(v) for v in self.lo]
+        a.hi[:] = [float(v) for v in self.hi]
+        a.cells, a.joint_idx, a.weights = ptr(self.d_cells), ptr(self.d_jidx), ptr(self.d_w)
+        a.coef, a.sigma = ptr(self.coef), ptr(self.sigma)
+        self._asset = a
+        h = C.c_void_p()
+        check(L.artemis_frame_create(C.byref(a), C.byref(h)), "frame_create")
+        self._h = h
+        self._outs = {}
+
+    # -- construction helpers -------------------------------------------------
+    @classmethod
+    def from_scene(cls, scene, **kw) -> "FramePipeline":
+        return cls(scene.cells, scene.skin_idx, scene.skin_w, scene.flut32, scene.degree,
+                   scene.channels, scene.resolution, scene.lo, scene.hi, rig=scene.rig, **kw)
+
+    @classmethod
+    def from_asset(cls, asset, **kw) -> "FramePipeline":
+        """From a reference CharacterAsset (render.py:106-126)."""
+        v = asset.voxels
+        rig = KM.Rig.from_any(asset.skeleton) if asset.skeleton is not None else None
+        if asset.weights is not None:
+            idx, w = asset.weights.joint_indices, asset.weights.weights
+        else:
+            idx = np.zeros((len(v.cells), 1), np.int32)
+            w = np.ones((len(v.cells), 1))
+        return cls(v.cells, idx, w, asset.flut.data, asset.flut.degree, asset.flut.channels,
+                   v.resolution, v.bounds.lo, v.bounds.hi, rig=rig, **kw)
+
+    # -- per frame --------------------------------------------------------------
+    def tables(self, pose) -> KM.PoseTables:
+        return KM.pose_tables(self.rig, KM.PoseSpec.from_any(pose), canonical=self._canon)
+
+    def camera(self, cam) -> _lib.Camera:
+        cam = KM.PinholeCamera.from_any(cam)
+        R, origin = cam.cam_to_world()
+        return K.camera_struct(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                               self.lo, self.cell)
+
+    def outputs(self, width: int, height: int):
+        key = (width, height)
+        if key not in self._outs:
+            with torch.cuda.stream(self.stream):
+                n = width * height
+                self._outs[key] = (empty((n, self.channels), np.float32), empty(n, np.float32),
+                                   empty(n, np.float32))
+        return self._outs[key]
+
+    def run(self, pose, camera, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
+            early_stop: bool = True, graph: bool = True, parity: bool = False, tables=None,
+            out=None):
+        """Enqueue one frame on self.stream; returns device (F, alpha, depth)
+        (fp32, row-major pixels). `pose` None renders the canonical cells."""
+        L = _lib.lib()
+        cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
+        if pose is None or self.rig is None:
+            aff = rot = None
+            nj = 1
+        else:
+            t = tables if tables is not None else self.tables(pose)
+            aff = np.ascontiguousarray(t.affine34)
+            rot = np.ascontiguousarray(t.rot_inv.reshape(-1, 9))
+            nj = int(aff.shape[0])
+        F, A, D = out if out is not None else self.outputs(cam.width, cam.height)
+        flags = (1 if early_stop else 0) | (2 if graph else 0) | (4 if parity else 0)
+        check(L.artemis_frame_run(self._h, aff.ctypes.data if aff is not None else None,
+                                  rot.ctypes.data if rot is not None else None, nj, C.byref(cam),
+                                  float(lambda_th), float(sigma_dep), flags, ptr(F), ptr(A),
+                                  ptr(D), self.stream.cuda_stream or None), "frame_run")
+        return F, A, D
+
+    def counts(self):
+        n_in, n_live = C.c_int64(), C.c_int64()
+        check(_lib.lib().artemis_frame_counts(self._h, C.byref(n_in), C.byref(n_live),
+                                              self.stream.cuda_stream or None), "frame_counts")
+        return int(n_in.value), int(n_live.value)
+
+    def profile(self, enable: bool = True) -> None:
+        check(_lib.lib().artemis_frame_profile(self._h, int(bool(enable))), "frame_profile")
+
+    def stage_ms(self) -> dict:
+        """Per-stage device ms of the last eager profiled run."""
+        ms = (C.c_float * 5)()
+        check(_lib.lib().artemis_frame_stage_ms(self._h, ms), "frame_stage_ms")
+        return dict(zip(("warp", "sort", "resolve", "build", "render"), [float(v) for v in ms]))
+
+    def launches_per_frame(self) -> int:
+        return int(_lib.lib().artemis_frame_launches(self._h))
+
+    def tree(self):
+        """Host copies of the last frame's tree (run with parity=True)."""
+        ft = _lib.FrameTree()
+        check(_lib.lib().artemis_frame_get_tree(self._h, C.byref(ft)), "frame_get_tree")
+        n_in, n_live = self.counts()
+
+        def grab(p, count, dtype, cols=1):
+            a = np.empty((max(count, 0), cols), dtype=dtype)
+            if count > 0:
+                check(_lib.lib().artemis_copy_to_host(a.ctypes.data, p, a.nbytes,
+                                                      self.stream.cuda_stream or None), "copy")
+            return a if cols > 1 else a.reshape(-1)
+
+        code_dt = np.uint32 if ft.code_bytes == 4 else np.uint64
+        out = dict(
+            n_in=n_in, n_live=n_live,
+            codes=grab(ft.codes, n_live, code_dt).astype(np.uint64),
+            flut_idx=grab(ft.flut_idx, n_live, np.uint32),
+            left=grab(ft.left, n_live - 1, np.int32),
+            right=grab(ft.right, n_live - 1, np.int32),
+            box_min=grab(ft.box_min, n_live - 1, np.int32, 3),
+            box_size=grab(ft.box_size, n_live - 1, np.int32, 3),
+            rotation_joint=grab(ft.rotation_joint, self.n, np.int32),
+        )
+        out["root"] = 0 if n_live > 1 else ~0
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().artemis_frame_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

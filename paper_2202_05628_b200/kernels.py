@@ -1,0 +1,288 @@
+"""The reference's flat-array kernel contract, on the B200.
+
+A module with the same names, argument meanings, dtypes and error
+behaviour as ``animvox._core`` / ``animvox._pure`` (selected by
+animvox/backend.py:19-31), so it can be bound as ``animvox.backend.kernels``
+(see install.py). Every call moves its numpy arguments to the device, runs
+the libartemis kernel through the C ABI and returns freshly allocated numpy
+arrays in the reference's dtypes:
+
+  morton_encode  _core.pyx:79-92     morton_decode  :95-105
+  sort_order     :111-167            build_tree     :193-246
+  traverse_ray   :358-389            render_rays    :473-559
+  forward_fit    :562-655
+
+``nthreads`` is accepted and ignored (results never depended on it).
+``backward_rays`` (training) is not on the
+frame path and is not provided by this module yet.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+from .device import download, empty, ptr, stream_handle, upload, workspace
+
+IS_COMPILED = True
+BACKEND = "artemis-b200"
+
+_MORTON_LIMIT = 1 << 21
+
+
+def morton_encode(coords):
+    arr = np.ascontiguousarray(coords, dtype=np.int64)
+    if arr.size and (arr.min() < 0 or arr.max() >= _MORTON_LIMIT):
+        raise ValueError("grid coordinates outside [0, 2^21)")
+    arr = arr.reshape(-1, 3)
+    n = arr.shape[0]
+    if n == 0:
+        return np.empty(0, dtype=np.uint64)
+    L = _lib.lib()
+    d_in = upload(arr, np.int64)
+    d_out = empty(n, np.uint64)
+    check(L.artemis_morton_encode(ptr(d_in), n, ptr(d_out), None, stream_handle()),
+          "morton_encode")
+    return download(d_out, np.uint64)
+
+
+def morton_decode(codes):
+    c = np.ascontiguousarray(codes, dtype=np.uint64).reshape(-1)
+    n = c.size
+    if n == 0:
+        return np.empty((0, 3), dtype=np.int64)
+    L = _lib.lib()
+    d_in = upload(c, np.uint64)
+    d_out = empty((n, 3), np.int64)
+    check(L.artemis_morton_decode(ptr(d_in), n, ptr(d_out), stream_handle()), "morton_decode")
+    return download(d_out)
+
+
+def sort_pairs_device(keys: torch.Tensor, vals: torch.Tensor | None, key_bits: int,
+                      key_bytes: int):
+    """Stable device sort of (key, value); returns (sorted keys, values)."""
+    L = _lib.lib()
+    n = keys.numel()
+    ws = workspace(L.artemis_sort_workspace_bytes(n, key_bits, key_bytes))
+    k_out = torch.empty_like(keys)
+    v_out = torch.empty(n, dtype=torch.int32, device=keys.device)
+    fn = L.artemis_sort_pairs_u32 if key_bytes == 4 else L.artemis_sort_pairs_u64
+    check(fn(ptr(keys), ptr(vals), ptr(k_out), ptr(v_out), n, key_bits, ptr(ws), ws.numel(),
+             stream_handle()), "sort")
+    return k_out, v_out
+
+
+def sort_order(codes, nthreads=1):
+    c = np.ascontiguousarray(codes, dtype=np.uint64).reshape(-1)
+    n = c.size
+    if n <= 1:
+        return np.arange(n, dtype=np.int64)
+    bits = max(1, int(c.max()).bit_length())
+    if bits <= 32:
+        keys = upload(c.astype(np.uint32), np.uint32)
+        _, perm = sort_pairs_device(keys, None, bits, 4)
+    else:
+        keys = upload(c, np.uint64)
+        _, perm = sort_pairs_device(keys, None, bits, 8)
+    return download(perm).astype(np.int64)
+
+
+def build_tree(codes, nthreads=1):
+    c = np.ascontiguousarray(codes, dtype=np.uint64).reshape(-1)
+    n = c.size
+    if n == 0:
+        raise ValueError("empty leaf set")
+    m = max(n - 1, 1)
+    if n == 1:
+        return (~0, np.empty(0, np.int32), np.empty(0, np.int32), np.empty((0, 3), np.int32),
+                np.empty((0, 3), np.int32))
+    L = _lib.lib()
+    d_c = upload(c, np.uint64)
+    left = empty(m, np.int32)
+    right = empty(m, np.int32)
+    bmin = empty((m, 3), np.int32)
+    bsize = empty((m, 3), np.int32)
+    check(L.artemis_build_tree(ptr(d_c), n, ptr(left), ptr(right), ptr(bmin), ptr(bsize), None,
+                               stream_handle()), "build_tree")
+    return 0, download(left), download(right), download(bmin), download(bsize)
+
+
+class DeviceTree:
+    """A reference-layout tree on the device plus its packed traversal copy."""
+
+    def __init__(self, codes, flut_idx, root, left, right, box_min, box_size):
+        c = np.ascontiguousarray(codes, dtype=np.uint64).reshape(-1)
+        n = c.size
+        if n < 1:
+            raise ValueError("empty leaf set")
+        L = _lib.lib()
+        self.n = n
+        self.codes = upload(c, np.uint64)
+        self.flut_idx = upload(np.asarray(flut_idx).reshape(-1), np.uint32)
+        if n > 1:
+            self.left = upload(left, np.int32)
+            self.right = upload(right, np.int32)
+            self.bmin = upload(np.asarray(box_min).reshape(-1, 3), np.int32)
+            self.bsize = upload(np.asarray(box_size).reshape(-1, 3), np.int32)
+        else:
+            self.left = self.right = self.bmin = self.bsize = None
+        self.nodes = workspace(32 * n)
+        check(L.artemis_pack_tree(ptr(self.codes), n, int(root), ptr(self.left), ptr(self.right),
+                                  ptr(self.bmin), ptr(self.bsize), ptr(self.nodes),
+                                  stream_handle()), "pack_tree")
+        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.flut_idx), n, None)
+
+
+class DeviceShading:
+    """FLUT split into fp32 coefficients + fp64 density, rotation tables."""
+
+    def __init__(self, flut, rot_index, rot_inv, degree, channels):
+        L = _lib.lib()
+        fl = np.asarray(flut)
+        if fl.ndim != 2:
+            raise ValueError("flut must be (N, H*C+1)")
+        n, width = fl.shape
+        self.coef = empty((n, max(width - 1, 1)), np.float32)
+        self.sigma = empty(n, np.float64)
+        if fl.dtype == np.float32:
+            d_fl = upload(fl, np.float32)
+            check(L.artemis_flut_split_f32(ptr(d_fl), n, width, ptr(self.coef), ptr(self.sigma),
+                                           stream_handle()), "flut_split")
+        else:
+            d_fl = upload(fl, np.float64)
+            check(L.artemis_flut_split_f64(ptr(d_fl), n, width, ptr(self.coef), ptr(self.sigma),
+                                           stream_handle()), "flut_split")
+        self.rot_index = upload(np.asarray(rot_index).reshape(-1), np.int32)
+        self.rot_inv = upload(np.asarray(rot_inv).reshape(-1, 9), np.float64)
+        self.view = _lib.Shading(ptr(self.coef), ptr(self.sigma), ptr(self.rot_index),
+                                 ptr(self.rot_inv), int(degree), int(channels), width - 1)
+
+
+class DeviceRays:
+    def __init__(self, origins_g, dirs_g, dirs_w, t_min, t_max):
+        self.og = upload(np.asarray(origins_g).reshape(-1, 3), np.float64)
+        self.dg = upload(np.asarray(dirs_g).reshape(-1, 3), np.float64)
+        self.dw = upload(np.asarray(dirs_w).reshape(-1, 3), np.float64) if dirs_w is not None \
+            else self.dg
+        self.n = self.og.shape[0]
+        self.view = _lib.Rays(ptr(self.og), ptr(self.dg), ptr(self.dw), self.n, float(t_min),
+                              float(t_max))
+
+    @staticmethod
+    def from_tensors(og, dg, dw, t_min=0.0, t_max=np.inf):
+        r = DeviceRays.__new__(DeviceRays)
+        r.og, r.dg, r.dw = og, dg, dw
+        r.n = og.shape[0]
+        r.view = _lib.Rays(ptr(og), ptr(dg), ptr(dw), r.n, float(t_min), float(t_max))
+        return r
+
+
+def render_device(tree: DeviceTree, shade: DeviceShading, rays: DeviceRays, lambda_th,
+                  sigma_dep, early_stop):
+    """Device tensors (F fp32 (R,C), alpha fp64, depth fp64)."""
+    L = _lib.lib()
+    C_ = shade.view.channels
+    F = empty((rays.n, C_), np.float32)
+    A = empty(rays.n, np.float64)
+    D = empty(rays.n, np.float64)
+    if rays.n:
+        check(L.artemis_render_rays(C.byref(tree.view), C.byref(shade.view), C.byref(rays.view),
+                                    float(lambda_th), float(sigma_dep), int(bool(early_stop)),
+                                    ptr(F), ptr(A), ptr(D), stream_handle()), "render_rays")
+    return F, A, D
+
+
+def render_rays(codes, flut_idx, root, left, right, box_min, box_size, origins_g, dirs_g,
+                dirs_w, t_min, t_max, flut, rot_index, rot_inv, degree, channels, lambda_th,
+                sigma_dep, early_stop, nthreads=1):
+    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size)
+    shade = DeviceShading(flut, rot_index, rot_inv, degree, channels)
+    rays = DeviceRays(origins_g, dirs_g, dirs_w, t_min, t_max)
+    F, A, D = render_device(tree, shade, rays, lambda_th, sigma_dep, early_stop)
+    return download(F).astype(np.float64), download(A), download(D)
+
+
+def count_hits_device(tree: DeviceTree, rays: DeviceRays) -> torch.Tensor:
+    L = _lib.lib()
+    counts = empty(rays.n, np.int64)
+    if rays.n:
+        check(L.artemis_count_hits(C.byref(tree.view), C.byref(rays.view), ptr(counts),
+                                   stream_handle()), "count_hits")
+    return counts
+
+
+def forward_fit_device(tree: DeviceTree, shade: DeviceShading, rays: DeviceRays):
+    """(F, alpha, offsets (host int64), hit_idx, hit_t0, hit_t1) device tensors."""
+    L = _lib.lib()
+    counts = download(count_hits_device(tree, rays))
+    offsets = np.zeros(rays.n + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    total = int(offsets[-1])
+    d_off = upload(offsets, np.int64)
+    hit_idx = empty(max(total, 1), np.int64)
+    hit_t0 = empty(max(total, 1), np.float64)
+    hit_t1 = empty(max(total, 1), np.float64)
+    F = empty((rays.n, shade.view.channels), np.float32)
+    A = empty(rays.n, np.float64)
+    if rays.n:
+        check(L.artemis_forward_fit(C.byref(tree.view), C.byref(shade.view), C.byref(rays.view),
+                                    ptr(d_off), ptr(hit_idx), ptr(hit_t0), ptr(hit_t1), ptr(F),
+                                    ptr(A), stream_handle()), "forward_fit")
+    return F, A, offsets, hit_idx[:total], hit_t0[:total], hit_t1[:total]
+
+
+def forward_fit(codes, flut_idx, root, left, right, box_min, box_size, origins_g, dirs_g,
+                dirs_w, t_min, t_max, flut, rot_index, rot_inv, degree, channels, nthreads=1):
+    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size)
+    shade = DeviceShading(flut, rot_index, rot_inv, degree, channels)
+    rays = DeviceRays(origins_g, dirs_g, dirs_w, t_min, t_max)
+    F, A, off, hi, h0, h1 = forward_fit_device(tree, shade, rays)
+    return (download(F).astype(np.float64), download(A), off, download(hi), download(h0),
+            download(h1))
+
+
+def traverse_ray(codes, flut_idx, root, left, right, box_min, box_size, origin_g, dir_g,
+                 t_min, t_max):
+    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size)
+    fi = np.asarray(flut_idx)
+    rows = int(fi.max()) + 1 if fi.size else 1
+    # trace-only: zero density and a 1-channel degree-0 table (no shading work)
+    shade = DeviceShading(np.zeros((rows, 2)), np.zeros(rows, np.int32), np.eye(3)[None], 0, 1)
+    rays = DeviceRays(np.asarray(origin_g).reshape(1, 3), np.asarray(dir_g).reshape(1, 3), None,
+                      t_min, t_max)
+    _, _, _, hi, h0, h1 = forward_fit_device(tree, shade, rays)
+    return download(hi), download(h0), download(h1)
+
+
+def camera_rays_device(R, origin, fx, fy, cx, cy, width, height, lo, cell):
+    """Exact device rays_for_camera + _grid_rays: (og, dg, dw) (W*H, 3) fp64."""
+    L = _lib.lib()
+    cam = camera_struct(R, origin, fx, fy, cx, cy, width, height, lo, cell)
+    n = width * height
+    og = empty((n, 3), np.float64)
+    dg = empty((n, 3), np.float64)
+    dw = empty((n, 3), np.float64)
+    check(L.artemis_camera_rays(C.byref(cam), ptr(og), ptr(dg), ptr(dw), stream_handle()),
+          "camera_rays")
+    return og, dg, dw
+
+
+def camera_struct(R, origin, fx, fy, cx, cy, width, height, lo, cell) -> _lib.Camera:
+    cam = _lib.Camera()
+    cam.R[:] = [float(v) for v in np.asarray(R, dtype=np.float64).reshape(9)]
+    cam.origin[:] = [float(v) for v in np.asarray(origin, dtype=np.float64)]
+    cam.fx, cam.fy, cam.cx, cam.cy = float(fx), float(fy), float(cx), float(cy)
+    cam.width, cam.height = int(width), int(height)
+    cam.lo[:] = [float(v) for v in np.asarray(lo, dtype=np.float64)]
+    cam.cell[:] = [float(v) for v in np.asarray(cell, dtype=np.float64)]
+    return cam
+
+
+def backward_rays(*args, **kwargs):
+    raise NotImplementedError(
+        "backward_rays (training gradients, animvox/_core.pyx:661-755) is the next row of "
+        "SURVEY.md section 8f and is not provided by the B200 frame path yet")

@@ -1,0 +1,285 @@
+"""GPU parity of the scene-level drop-ins and the device frame pipeline
+against the reference (golden fixtures from running it) and the oracle.
+
+Bit-exact: warped positions, live cells, in-bounds flags, rotation joints,
+collision groups, resolve winners and pairs, Morton keys and every tree
+array, per-ray hit traces. Tolerance: F within 1e-4 max / 1e-5 mean-abs,
+alpha within 1e-6 (fp32 output of the frame pipeline) or 1e-9 (fp64 API).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2202_05628_b200 import kinematics as KM
+from paper_2202_05628_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+F_MAX, F_MEAN = 1e-4, 1e-5
+
+
+def digest(a) -> str:
+    a = np.ascontiguousarray(np.asarray(a))
+    h = hashlib.sha256()
+    h.update(str(a.dtype).encode())
+    h.update(str(a.shape).encode())
+    h.update(a.tobytes())
+    return h.hexdigest()
+
+
+class Vox:
+    """Duck-typed VoxelSet / SkinWeights / FLUT / Bounds built from a Scene."""
+
+    def __init__(self, sc):
+        from paper_2202_05628_b200.types import Bounds
+
+        self.resolution = sc.resolution
+        self.bounds = Bounds(sc.lo, sc.hi)
+        self.cells = sc.cells
+
+
+class Weights:
+    def __init__(self, sc):
+        self.joint_indices = sc.skin_idx
+        self.weights = sc.skin_w
+
+
+class Flut:
+    def __init__(self, sc):
+        self.data = sc.flut64()
+        self.degree = sc.degree
+        self.channels = sc.channels
+
+    def __len__(self):
+        return self.data.shape[0]
+
+    @property
+    def densities(self):
+        return self.data[:, -1]
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2202_05628_b200 import pipeline
+
+    return pipeline
+
+
+@pytest.fixture(scope="module")
+def mini():
+    return S.make_scene("c0", resolution=64, image=(64, 64))
+
+
+@pytest.fixture(scope="module")
+def c0():
+    return S.make_scene("c0")
+
+
+def groups_csr(groups):
+    off = np.zeros(len(groups) + 1, dtype=np.int64)
+    if groups:
+        off[1:] = np.cumsum([g.size for g in groups])
+    mem = np.concatenate(groups) if groups else np.zeros(0, dtype=np.int64)
+    return off, mem
+
+
+def check_warp(P, sc, g):
+    pose = KM.PoseSpec.make(sc.poses[0])
+    warp = P.warp_voxels(Vox(sc), Weights(sc), sc.rig, pose)
+    off, mem = groups_csr(warp.collision_groups)
+    got = {"warp_positions": warp.positions, "warp_cells": warp.cells,
+           "warp_in_bounds": warp.in_bounds, "warp_rotation_joint": warp.rotation_joint,
+           "warp_rotations": warp.rotations, "groups_off": off, "groups_mem": mem}
+    bad = [k for k, v in got.items() if digest(v) != str(g[f"sha_{k}"])]
+    assert not bad, bad
+    return warp
+
+
+class TestDropIns:
+    def test_warp_mini(self, P, mini, golden_mini):
+        check_warp(P, mini, golden_mini)
+
+    def test_warp_c0(self, P, c0, golden_c0):
+        check_warp(P, c0, golden_c0)
+
+    def test_resolve_and_build(self, P, c0, golden_c0):
+        g = golden_c0
+        warp = check_warp(P, c0, g)
+        res = P.resolve_collisions(warp, Flut(c0))
+        for k, v in {"res_cells": res.cells, "res_flut": res.flut_indices,
+                     "res_pairs": res.pairs}.items():
+            assert digest(v) == str(g[f"sha_{k}"]), k
+        oc = P.build_octree(res.cells, res.flut_indices, resolution=c0.resolution,
+                            bounds=Vox(c0).bounds)
+        assert oc.root == int(g["oct_root"])
+        for k, v in {"oct_codes": oc.codes, "oct_flut": oc.flut_idx, "oct_left": oc.left,
+                     "oct_right": oc.right, "oct_bmin": oc.box_min,
+                     "oct_bsize": oc.box_size}.items():
+            assert digest(v) == str(g[f"sha_{k}"]), k
+
+    def test_render_view_mini(self, P, mini, golden_mini):
+        g = golden_mini
+        sc = mini
+        warp = check_warp(P, sc, g)
+        res = P.resolve_collisions(warp, Flut(sc))
+        oc = P.build_octree(res.cells, res.flut_indices, resolution=sc.resolution,
+                            bounds=Vox(sc).bounds)
+        from paper_2202_05628_b200.types import RenderOptions
+
+        fb = P.render_view(oc, Flut(sc), warp, sc.cameras[0][0],
+                           RenderOptions(lambda_th=1e-4, sigma_dep=5.0))
+        err = np.abs(fb.features - g["F"])
+        assert err.max() <= F_MAX and err.mean() <= F_MEAN
+        assert np.max(np.abs(fb.alpha - g["A"])) <= 1e-9
+        assert digest(fb.depth) == str(g["sha_depth"])
+
+    def test_duplicate_cells_rejected(self, P):
+        from paper_2202_05628_b200.errors import DuplicateMortonError
+        from paper_2202_05628_b200.types import Bounds
+
+        with pytest.raises(DuplicateMortonError):
+            P.build_octree(np.array([[1, 2, 3], [1, 2, 3]], dtype=np.int32), resolution=8,
+                           bounds=Bounds(np.zeros(3), np.ones(3)))
+
+    def test_collision_policy_ties(self, P):
+        """rigging.py resolve: max sigma wins, ties to the lowest index,
+        pairs in (-sigma, index) order (test_rigging.py:420-481 shape)."""
+        from paper_2202_05628_b200 import types as T
+
+        rng = np.random.default_rng(20)
+        n = 1000
+        cells = (2 + rng.integers(0, 5, size=(n, 3))).astype(np.int32)
+        sigma = np.round(rng.uniform(0.0, 10.0, n), 1)  # many exact ties
+        warp = T.WarpResult(16, np.zeros(3), np.full(3, 1 / 16), np.zeros((n, 3)), cells,
+                            np.zeros((n, 4)), np.zeros(n, np.int32), np.eye(3)[None],
+                            np.ones(n, bool), ())
+
+        class F:
+            densities = sigma
+
+        res = P.resolve_collisions(warp, F)
+        live, win, pairs = oracle.resolve(cells, np.ones(n, bool), sigma)
+        assert np.array_equal(res.cells, live)
+        assert np.array_equal(res.flut_indices, win)
+        assert np.array_equal(res.pairs, pairs)
+
+    def test_all_out_of_bounds(self, P):
+        from paper_2202_05628_b200 import types as T
+
+        warp = T.WarpResult(8, np.zeros(3), np.full(3, 0.125), np.zeros((4, 3)),
+                            -np.ones((4, 3), np.int32), np.zeros((4, 4)), np.zeros(4, np.int32),
+                            np.eye(3)[None], np.zeros(4, bool), ())
+
+        class F:
+            densities = np.ones(4)
+
+        res = P.resolve_collisions(warp, F)
+        assert res.cells.shape == (0, 3) and res.pairs.shape == (0, 2)
+
+
+class TestFramePipeline:
+    def _frame_vs_golden(self, sc, g, graph):
+        from paper_2202_05628_b200.frame import FramePipeline
+
+        fp = FramePipeline.from_scene(sc)
+        pose = KM.PoseSpec.make(sc.poses[0])
+        cam = sc.cameras[0][0]
+        for _ in range(2):  # second run replays the captured graph
+            F, A, D = fp.run(pose, cam, lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep,
+                             graph=graph, parity=True)
+        fp.stream.synchronize()
+        t = fp.tree()
+        assert t["n_live"] == int(g["n_leaves"])
+        assert t["n_in"] == int(g["n_inbounds"])
+        assert t["root"] == int(g["oct_root"])
+        for k, v in {"oct_codes": t["codes"], "oct_flut": t["flut_idx"], "oct_left": t["left"],
+                     "oct_right": t["right"], "oct_bmin": t["box_min"],
+                     "oct_bsize": t["box_size"],
+                     "warp_rotation_joint": t["rotation_joint"]}.items():
+            assert digest(v) == str(g[f"sha_{k}"]), k
+        pix = g["sub_pix"]
+        Fh = F.cpu().numpy()[pix].astype(np.float64)
+        err = np.abs(Fh - g["sub_F"])
+        assert err.max() <= F_MAX and err.mean() <= F_MEAN
+        assert np.max(np.abs(A.cpu().numpy()[pix] - g["sub_A"])) <= 1e-6
+        Dh = D.cpu().numpy()[pix]
+        want = g["sub_D"].astype(np.float32)
+        assert np.array_equal(Dh, want)
+        fp.close()
+
+    @pytest.mark.parametrize("graph", [False, True])
+    def test_c0_frame(self, c0, golden_c0, graph):
+        self._frame_vs_golden(c0, golden_c0, graph)
+
+    def test_c2_frame(self, golden_c2):
+        self._frame_vs_golden(S.make_scene("c2"), golden_c2, True)
+
+    def test_graph_replay_equals_eager_over_poses(self):
+        from paper_2202_05628_b200.frame import FramePipeline
+
+        sc = S.make_scene("c3", resolution=128, shell=3, scale=0.76, channels=16,
+                          image=(256, 256), frames=4)
+        fp = FramePipeline.from_scene(sc)
+        for f in range(4):
+            pose = KM.PoseSpec.make(sc.poses[f])
+            cam = sc.cameras[f][0]
+            Fg, Ag, Dg = [x.clone() for x in fp.run(pose, cam, graph=True)]
+            Fe, Ae, De = [x.clone() for x in fp.run(pose, cam, graph=False)]
+            fp.stream.synchronize()
+            assert (Fg == Fe).all() and (Ag == Ae).all() and (Dg == De).all()
+            # and against the oracle frame
+            tables = KM.pose_tables(sc.rig, pose)
+            want = oracle.render_frame(sc, tables, cam)
+            err = np.abs(Fg.cpu().numpy().astype(np.float64) - want["F"])
+            assert err.max() <= F_MAX and err.mean() <= F_MEAN
+        fp.close()
+
+    def test_identity_pose(self, mini):
+        """pose None renders the canonical cells (render.py:162-167)."""
+        from paper_2202_05628_b200.frame import FramePipeline
+
+        fp = FramePipeline.from_scene(mini)
+        cam = mini.cameras[0][0]
+        F, A, D = fp.run(None, cam, graph=False, parity=True)
+        fp.stream.synchronize()
+        tree = oracle.build_octree(mini.cells)
+        t = fp.tree()
+        assert np.array_equal(t["codes"], tree[0])
+        assert np.array_equal(t["flut_idx"], tree[1])
+        tables = KM.identity_tables()
+        R, origin = cam.cam_to_world()
+        og, dg, dw = oracle.camera_rays(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
+                                        cam.height, mini.lo, mini.cell_size)
+        Fw, Aw, Dw = oracle.render_rays(*tree, og, dg, dw, 0.0, np.inf, mini.flut64(),
+                                        np.zeros(mini.n_voxels, np.int32), tables.rot_inv,
+                                        mini.degree, mini.channels, 1e-4, 5.0, True)
+        err = np.abs(F.cpu().numpy().astype(np.float64) - Fw)
+        assert err.max() <= F_MAX and err.mean() <= F_MEAN
+        fp.close()
+
+    def test_everything_warped_out(self, mini):
+        """A pose that moves every voxel out of the grid renders an empty
+        frame (EmptyWarpError at the Python layer, render.py:170-171)."""
+        from paper_2202_05628_b200.frame import FramePipeline
+
+        fp = FramePipeline.from_scene(mini)
+        pose = KM.PoseSpec.make(np.zeros((mini.rig.n_joints, 3)), g_trans=[100.0, 0.0, 0.0])
+        F, A, D = fp.run(pose, mini.cameras[0][0], graph=False)
+        fp.stream.synchronize()
+        assert fp.counts() == (0, 0)
+        assert float(A.abs().max()) == 0.0 and float(F.abs().max()) == 0.0
+        fp.close()
+
+    def test_camera_rays_bit_exact(self, c0, golden_c0):
+        from paper_2202_05628_b200 import kernels as K
+
+        cam = c0.cameras[0][0]
+        R, origin = cam.cam_to_world()
+        og, dg, dw = K.camera_rays_device(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
+                                          cam.height, c0.lo, c0.cell_size)
+        assert digest(dw.cpu().numpy()) == str(golden_c0["sha_rays_d"])
