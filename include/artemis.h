@@ -91,11 +91,12 @@ int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *left, int32_t 
  * The render kernels walk a packed copy of the tree: one 32-byte record per
  * internal node holding both children's boxes (so a visit is one sector),
  * plus a super-root record at index max(n-1, 0) whose left child is the
- * root. Built from the reference arrays (API path) or directly by
- * artemis_frame_run (device pipeline). nodes: (n) x 32 bytes. */
-int artemis_pack_tree(const uint64_t *codes, int64_t n, int32_t root, const int32_t *left,
-                      const int32_t *right, const int32_t *box_min, const int32_t *box_size,
-                      void *nodes, artemis_stream stream);
+ * root, and one 16-byte record per leaf {x, y, z, flut row}. Built from the
+ * reference arrays (API path) or directly by artemis_frame_run (device
+ * pipeline). nodes: n x 32 bytes, leaves: n x 16 bytes. */
+int artemis_pack_tree(const uint64_t *codes, const uint32_t *flut_idx, int64_t n, int32_t root,
+                      const int32_t *left, const int32_t *right, const int32_t *box_min,
+                      const int32_t *box_size, void *nodes, void *leaves, artemis_stream stream);
 
 /* FLUT (n, width) row-major -> fp32 coefficients (n, width-1) + fp64
  * density (n). Replaces the FLUT.data gather layout of _core.pyx:536-551. */
@@ -105,8 +106,8 @@ int artemis_flut_split_f32(const float *flut, int64_t n, int width, float *coef,
                            double *sigma, artemis_stream stream);
 
 typedef struct {
-    const void *nodes;          /* artemis_pack_tree output */
-    const uint32_t *flut_idx;   /* (n_leaves) leaf -> FLUT row */
+    const void *nodes;          /* artemis_pack_tree output: internal records */
+    const void *leaves;         /* artemis_pack_tree output: leaf records */
     int64_t n_leaves;           /* host value; ignored when n_leaves_dev != NULL */
     const int32_t *n_leaves_dev;/* device count (device pipeline), may be NULL */
 } artemis_tree_view;

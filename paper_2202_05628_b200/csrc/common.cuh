@@ -70,10 +70,19 @@ __host__ __device__ __forceinline__ u64 morton3(u64 x, u64 y, u64 z) {
 // One internal node = 32 bytes: both children's octant boxes (min corner
 // plus the number of free Morton bits, which fixes the per-axis power-of-two
 // size exactly as _core.pyx:182-190 does) and the child links.
-// word[0] = L.x | L.free << 21, word[1] = L.y, word[2] = L.z, word[3] = left
-// word[4] = R.x | R.free << 21, word[5] = R.y, word[6] = R.z, word[7] = right
-// A child with free == kAbsent does not exist (the super-root's right).
-constexpr uint32_t kAbsent = 0x7FF;
+// word[0] = L.x | L.free << 21 | split_axis << 27, word[1] = L.y,
+// word[2] = L.z, word[3] = left
+// word[4] = R.x | R.free << 21 | absent << 31, word[5] = R.y, word[6] = R.z,
+// word[7] = right
+// split_axis is the axis of the node's highest differing Morton bit: the
+// plane that separates the two children's octants. kAbsent marks a missing
+// child (the super-root's right).
+constexpr uint32_t kAbsent = 1u << 31;
+constexpr uint32_t kCoordMask = 0x1FFFFFu;
+
+__host__ __device__ __forceinline__ int split_axis_of(int free_bits) {
+    return (free_bits - 1) % 3;
+}
 
 struct PackedNode {
     uint32_t w[8];

@@ -27,7 +27,7 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, double lambda_th,
                   double sigma_dep, int early_stop, float *F, float *A, float *D,
-                  cudaStream_t st);
+                  unsigned long long *queue, cudaStream_t st);
 
 constexpr int kMaxFrameJoints = 256;
 
@@ -52,6 +52,7 @@ struct artemis_frame_s {
     int32_t *rot_joint = nullptr, *counters = nullptr;
     int32_t *left = nullptr, *right = nullptr, *bmin = nullptr, *bsize = nullptr;
     PackedNode *nodes = nullptr;
+    uint4 *leaves = nullptr;
     void *sort_ws = nullptr, *resolve_ws = nullptr;
     size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
     FrameParams *params = nullptr;
@@ -91,7 +92,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         if (prof) cudaEventRecord(f->ev[k], st);
     };
     mark(0);
-    ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 2 * sizeof(int32_t), st));
+    // counters: [0] in-bounds, [1] live leaves, [2..3] render ray queue (u64)
+    ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 4 * sizeof(int32_t), st));
     rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,
                        identity ? 1 : n_joints, f->lo, f->cell, as.resolution, f->key_bytes,
                        f->keys, f->vals, f->rot_joint, f->counters, f->sentinel, identity, st);
@@ -112,7 +114,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         mark(3);
         rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
                                          f->n, write_ref ? f->left : nullptr, f->right, f->bmin,
-                                         f->bsize, f->nodes, nullptr, st);
+                                         f->bsize, f->nodes, f->leaves, f->winners, nullptr, st);
     } else {
         rc = sort_pairs<u64>((const u64 *)f->keys, f->vals, (u64 *)f->keys_sorted, f->vals_sorted,
                              f->n, f->key_bits, f->sort_ws, f->sort_ws_bytes, st);
@@ -125,17 +127,18 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         mark(3);
         rc = launch_build_tree<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n,
                                     write_ref ? f->left : nullptr, f->right, f->bmin, f->bsize,
-                                    f->nodes, nullptr, st);
+                                    f->nodes, f->leaves, f->winners, nullptr, st);
     }
     if (rc) return rc;
     mark(4);
     const int passes = f->key_bits <= 0 ? 1 : (f->key_bits + 7) / 8;
     launches += 2 + passes + 3 + 1;
-    artemis_tree_view tv{f->nodes, f->winners, 0, f->counters + 1};
+    artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, lambda_th, sigma_dep,
-                       flags & 1, F, A, D, st);
+                       flags & 1, F, A, D,
+                       reinterpret_cast<unsigned long long *>(f->counters + 2), st);
     mark(5);
     launches += 1;
     f->launches = launches;
@@ -178,6 +181,7 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->bmin, n * 12);
     rc = rc ? rc : dev_alloc(&f->bsize, n * 12);
     rc = rc ? rc : dev_alloc(&f->nodes, (n + 1) * sizeof(PackedNode));
+    rc = rc ? rc : dev_alloc(&f->leaves, (n + 1) * sizeof(uint4));
     f->sort_ws_bytes = sort_workspace_bytes(n, f->key_bits, f->key_bytes);
     f->resolve_ws_bytes = resolve_workspace_bytes(n);
     rc = rc ? rc : dev_alloc(&f->sort_ws, f->sort_ws_bytes);
@@ -198,6 +202,7 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
         if (e) cudaEventDestroy(e);
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
+                    f->leaves,
                     f->sort_ws, f->resolve_ws, f->params};
     for (void *b : bufs)
         if (b) cudaFree(b);

@@ -33,14 +33,17 @@ namespace artemis {
 namespace {
 constexpr int kRenderWarps = 4;
 constexpr int kRenderThreads = 32 * kRenderWarps;
-constexpr int kStack = 68;  // depth <= 64 key bits + super-root + far siblings
+constexpr int kSmemStack = 32;       // per-thread stack entries kept in shared memory
+constexpr int kStack = 68;           // tree depth <= 64 key bits + super-root; overflow in local
+constexpr int kStackBytes = kSmemStack * kRenderThreads * 4;
+constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~leaf)
 }  // namespace
 
 enum RenderMode { kRender = 0, kTrace = 1, kCount = 2 };
 
 struct RenderArgs {
     const PackedNode *nodes;
-    const uint32_t *leaf_flut;
+    const uint4 *leaves;  // {x, y, z, flut row}
     int64_t n_leaves;
     const int32_t *n_leaves_dev;
     // shading
@@ -54,7 +57,8 @@ struct RenderArgs {
     const double *og, *dg, *dw;
     const artemis_camera *cam;
     int64_t n_rays;
-    int tiles_x;  // camera mode: ceil(W / 8)
+    int tiles_x, tiles_y;  // camera mode: ceil(W / 8), ceil(H / 4)
+    unsigned long long *queue;  // ray-id counter, zero at launch
     double t_min, t_max;
     double stop;  // 1 - lambda_th
     double sigma_dep;
@@ -71,11 +75,11 @@ struct RenderArgs {
 
 // Ray/box overlap of the child box packed in (w0, w1, w2) within
 // [t_min, t_max]; exact port of the slab test (_core.pyx:252-285).
-__device__ __forceinline__ bool clip_child(uint32_t w0, uint32_t w1, uint32_t w2,
+__device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2,
                                            const double o[3], const double d[3], double t_min,
                                            double t_max, double &t0o, double &t1o) {
-    const int fb = (int)(w0 >> 21);
-    const int lo_i[3] = {(int)(w0 & 0x1FFFFFu), (int)w1, (int)w2};
+    const int fb = (int)((w0 >> 21) & 63u);
+    const int lo_i[3] = {(int)(w0 & kCoordMask), (int)(w1 & kCoordMask), (int)(w2 & kCoordMask)};
     double t0 = t_min, t1 = t_max;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -101,64 +105,36 @@ __device__ __forceinline__ bool clip_child(uint32_t w0, uint32_t w1, uint32_t w2
     return true;
 }
 
-struct RayWalk {
-    int stk[kStack];
-    double s0[kStack], s1[kStack];
-    int top;
-
-    __device__ __forceinline__ void expand(const PackedNode *nodes, int node, const double o[3],
-                                           const double d[3], double t_min, double t_max) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(nodes + node));
-        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(nodes + node) + 1);
-        double l0, l1, r0, r1;
-        const bool hl = clip_child(a.x, a.y, a.z, o, d, t_min, t_max, l0, l1);
-        const bool hr = (b.x >> 21) != kAbsent && clip_child(b.x, b.y, b.z, o, d, t_min, t_max, r0, r1);
-        const int l = (int)a.w, r = (int)b.w;
-        // push the far child first so the near one pops next (_core.pyx:338-354)
-        if (hl && hr) {
-            if (l0 <= r0) {
-                push(r, r0, r1);
-                push(l, l0, l1);
-            } else {
-                push(l, l0, l1);
-                push(r, r0, r1);
-            }
-        } else if (hl) {
-            push(l, l0, l1);
-        } else if (hr) {
-            push(r, r0, r1);
+// Filtered hit test: the slab planes are scaled by a per-ray reciprocal
+// instead of divided, which is within 3 ulp of the exact quotient; the
+// decision t0 < t1 is taken from it only when the gap exceeds a bound far
+// above that error (2^-50 relative), otherwise the exact test decides. So
+// the answer always equals clip_exact's; only its cost differs.
+__device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t w2,
+                                             const double o[3], const double d[3],
+                                             const double inv[3], double t_min, double t_max) {
+    const int fb = (int)((w0 >> 21) & 63u);
+    const int lo_i[3] = {(int)(w0 & kCoordMask), (int)(w1 & kCoordMask), (int)(w2 & kCoordMask)};
+    double t0 = t_min, t1 = t_max;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double lo = (double)lo_i[a];
+        const double hi = (double)(lo_i[a] + box_size_axis(fb, a));
+        if (d[a] == 0.0) {
+            if (o[a] < lo || o[a] >= hi) return false;
+        } else {
+            double ta = (lo - o[a]) * inv[a];
+            double tb = (hi - o[a]) * inv[a];
+            t0 = fmax(t0, fmin(ta, tb));
+            t1 = fmin(t1, fmax(ta, tb));
         }
     }
-    __device__ __forceinline__ void push(int n, double t0, double t1) {
-        stk[top] = n;
-        s0[top] = t0;
-        s1[top] = t1;
-        ++top;
-    }
-    // Next occupied leaf front to back; false when the ray is exhausted.
-    __device__ __forceinline__ bool next(const PackedNode *nodes, const double o[3],
-                                         const double d[3], double t_min, double t_max, int &leaf,
-                                         double &t0, double &t1) {
-        while (top > 0) {
-            --top;
-            const int node = stk[top];
-            if (node < 0) {
-                t0 = s0[top];
-                t1 = s1[top];
-                if (t1 > t0) {
-                    leaf = ~node;
-                    return true;
-                }
-                continue;
-            }
-            // internal nodes were tested when their parent was expanded;
-            // the reference's re-test on pop (_core.pyx:332) repeats the same
-            // computation on the same inputs and is skipped.
-            expand(nodes, node, o, d, t_min, t_max);
-        }
-        return false;
-    }
-};
+    const double m = 8.881784197001252e-16 * (fabs(t0) + (isinf(t1) ? 0.0 : fabs(t1)));
+    if (t0 + m < t1) return true;
+    if (t0 > t1 + m) return false;
+    double e0, e1;
+    return clip_exact(w0, w1, w2, o, d, t_min, t_max, e0, e1);
+}
 
 template <int kDeg>
 __device__ __forceinline__ void sh_basis_f(float x, float y, float z, float *Y) {
@@ -217,172 +193,328 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
     }
 }
 
-template <int kDeg, int kMode, bool kCamera>
+// Persistent warps pull rays from a global queue (ids in 8x4 pixel-tile order
+// in camera mode) and refill idle lanes as rays finish, so SIMD lanes stay
+// busy despite the ~6x spread of per-ray work. Each lane walks its ray's
+// DFS with a stack in shared memory (column per thread, so lanes at
+// different depths never bank-conflict). Child visiting order uses the
+// split axis: the two children's octants are separated by the plane of the
+// node's highest differing Morton bit, so when both are hit the one on the
+// ray's side of that plane has the smaller entry distance -- the order the
+// reference's `lt0 <= rt0` comparison yields (_core.pyx:345), without
+// computing either distance. Internal-node tests use the filtered predicate;
+// emitted leaves get exact fp64 intervals. Visible hits of a round are then
+// shaded by lane groups.
+template <int kDeg, int kMode, bool kCamera, bool kVec>
 __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
     constexpr int H = (kDeg + 1) * (kDeg + 1);
-    extern __shared__ float s_feat[];  // [warps][32 rays][C | 1]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    int *s_stack = reinterpret_cast<int *>(s_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
-    const int cstride = C | 1;
-    float *feat = s_feat + (size_t)warp * 32 * cstride;
+    const int cp = kVec ? C + 4 : (C | 1);
+    float *feat = reinterpret_cast<float *>(s_raw + kStackBytes) + (size_t)warp * 32 * cp;
     if (kMode != kCount)
-        for (int i = lane; i < 32 * cstride; i += 32) feat[i] = 0.0f;
+        for (int i = lane; i < 32 * cp; i += 32) feat[i] = 0.0f;
+    const int64_t n_leaves = p.n_leaves_dev ? (int64_t)*p.n_leaves_dev : p.n_leaves;
+    const int super_root = (int)(n_leaves > 1 ? n_leaves - 1 : 0);
+    const int64_t n_ids = kCamera ? (int64_t)p.tiles_x * p.tiles_y * 32 : p.n_rays;
+    const unsigned lt = lanemask_lt();
 
-    const int64_t gwarp = blockIdx.x * (int64_t)kRenderWarps + warp;
+    // per-lane ray state
     int64_t ray = -1;
-    double og[3], dg[3], dw[3];
-    if (kCamera) {
-        const artemis_camera &cam = *p.cam;
-        const int tx = (int)(gwarp % p.tiles_x), ty = (int)(gwarp / p.tiles_x);
-        const int px = tx * 8 + (lane & 7), py = ty * 4 + (lane >> 3);
-        if (py < cam.height && px < cam.width) {
-            ray = (int64_t)py * cam.width + px;
-            camera_ray(cam, px, py, og, dg, dw);
+    bool alive = false;
+    double og[3], dg[3], dw[3], inv[3];
+    double T = 1.0, acc = 0.0, depth = CUDART_INF;
+    int64_t hits = 0, trace_base = 0;
+    int cur = kEnd, top = 0;
+    int ovf[kStack - kSmemStack];
+    bool queue_open = true;
+
+    auto push = [&](int v) {
+        if (top < kSmemStack)
+            s_stack[top * kRenderThreads + tid] = v;
+        else
+            ovf[top - kSmemStack] = v;
+        ++top;
+    };
+    auto pop = [&]() -> int {
+        if (top == 0) return kEnd;
+        --top;
+        return top < kSmemStack ? s_stack[top * kRenderThreads + tid] : ovf[top - kSmemStack];
+    };
+    // next occupied leaf front to back (_core.pyx:307-355 order)
+    auto next_hit = [&](int &leaf, double &t0, double &t1, uint32_t &fidx) -> bool {
+        while (cur != kEnd) {
+            if (cur >= 0) {
+                const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur));
+                const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur) + 1);
+                const bool hl = hit_filtered(a.x, a.y, a.z, og, dg, inv, p.t_min, p.t_max);
+                const bool hr = !(b.x & kAbsent) &&
+                                hit_filtered(b.x, b.y, b.z, og, dg, inv, p.t_min, p.t_max);
+                int nxt;
+                uint4 nb;
+                if (hl && hr) {
+                    const bool left_first = dg[(a.x >> 27) & 3u] > 0.0;
+                    push(left_first ? (int)b.w : (int)a.w);
+                    nb = left_first ? a : b;
+                } else if (hl) {
+                    nb = a;
+                } else if (hr) {
+                    nb = b;
+                } else {
+                    cur = pop();
+                    continue;
+                }
+                nxt = (int)nb.w;
+                if (nxt >= 0) {
+                    cur = nxt;  // internal nodes were just tested: expand directly
+                    continue;
+                }
+                cur = pop();
+                double e0, e1;
+                if (clip_exact(nb.x, nb.y, nb.z, og, dg, p.t_min, p.t_max, e0, e1) && e1 > e0) {
+                    leaf = ~nxt;
+                    t0 = e0;
+                    t1 = e1;
+                    fidx = __ldg(&p.leaves[leaf].w);
+                    return true;
+                }
+                continue;
+            }
+            leaf = ~cur;
+            const uint4 L = __ldg(p.leaves + leaf);
+            cur = pop();
+            double e0, e1;
+            if (clip_exact(L.x, L.y, L.z, og, dg, p.t_min, p.t_max, e0, e1) && e1 > e0) {
+                t0 = e0;
+                t1 = e1;
+                fidx = L.w;
+                return true;
+            }
         }
-    } else {
-        const int64_t r = gwarp * 32 + lane;
-        if (r < p.n_rays) {
-            ray = r;
+        return false;
+    };
+    auto start_ray = [&](int64_t id) {
+        ray = -1;
+        if (kCamera) {
+            const artemis_camera &cam = *p.cam;
+            const int64_t tile = id >> 5;
+            const int sl = (int)(id & 31);
+            const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
+            const int py = (int)(tile / p.tiles_x) * 4 + (sl >> 3);
+            if (py < cam.height && px < cam.width) {
+                ray = (int64_t)py * cam.width + px;
+                camera_ray(cam, px, py, og, dg, dw);
+            }
+        } else {
+            ray = id;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                og[a] = p.og[3 * r + a];
-                dg[a] = p.dg[3 * r + a];
-                dw[a] = p.dw[3 * r + a];
+                og[a] = p.og[3 * id + a];
+                dg[a] = p.dg[3 * id + a];
+                dw[a] = p.dw[3 * id + a];
             }
         }
-    }
-    const int64_t n_leaves = p.n_leaves_dev ? (int64_t)*p.n_leaves_dev : p.n_leaves;
-    bool alive = ray >= 0 && n_leaves > 0;
+        if (ray < 0) return;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) inv[a] = dg[a] != 0.0 ? 1.0 / dg[a] : 0.0;
+        T = 1.0;
+        acc = 0.0;
+        depth = CUDART_INF;
+        hits = 0;
+        top = 0;
+        trace_base = (kMode == kTrace) ? p.offsets[ray] : 0;
+        cur = n_leaves > 0 ? super_root : kEnd;
+        alive = true;
+    };
+    auto finish_ray = [&]() {
+        if (kMode == kCount) {
+            p.counts[ray] = hits;
+        } else {
+            if (p.A64) p.A64[ray] = acc;
+            if (p.A32) p.A32[ray] = (float)acc;
+            if (kMode == kRender) {
+                if (p.D64) p.D64[ray] = depth;
+                if (p.D32) p.D32[ray] = (float)depth;
+            }
+        }
+    };
 
-    RayWalk walk;
-    walk.top = 0;
-    if (alive) walk.expand(p.nodes, (int)(n_leaves > 1 ? n_leaves - 1 : 0), og, dg, p.t_min, p.t_max);
-
-    double T = 1.0, acc = 0.0, depth = CUDART_INF;
-    int64_t hits = 0;
-    const int64_t trace_base = (kMode == kTrace && ray >= 0) ? p.offsets[ray] : 0;
-
-    // group geometry for cooperative shading
-    int gs = 1;
-    while (gs < C && gs < 32) gs <<= 1;
-    const int hpr = 32 / gs;  // hits shaded per round
-    const int sub = lane / gs, ch0 = lane % gs;
+    // cooperative shading geometry: lph lanes per hit, hpi hits per pass
+    const int units = kVec ? C / 4 : C;
+    int lph = 1;
+    while (lph < units && lph < 32) lph <<= 1;
+    const int hpi = 32 / lph;
+    const int grp = lane / lph, q = lane % lph;
 
     while (true) {
-        int leaf = 0;
-        double t0 = 0.0, t1 = 0.0;
-        bool have = false;
-        if (alive) {
-            have = walk.next(p.nodes, og, dg, p.t_min, p.t_max, leaf, t0, t1);
-            if (!have) alive = false;
+        // ---- refill idle lanes from the ray queue
+        const unsigned idle = __ballot_sync(0xffffffffu, ray < 0);
+        if (queue_open && __popc(idle) >= 8) {
+            int64_t base = 0;
+            if (lane == 0) base = (int64_t)atomicAdd(p.queue, (unsigned long long)__popc(idle));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= n_ids) queue_open = false;
+            if (ray < 0) {
+                const int64_t id = base + __popc(idle & lt);
+                if (id < n_ids) start_ray(id);
+            }
         }
-        if (kMode == kCount) {
-            hits += have;
-            if (__ballot_sync(0xffffffffu, alive) == 0) break;
+        if (__ballot_sync(0xffffffffu, ray >= 0) == 0) {
+            if (!queue_open) break;
             continue;
         }
-        bool shade = false;
+        // ---- one traversal step per live lane
+        int leaf = 0;
+        double t0 = 0.0, t1 = 0.0;
         uint32_t fidx = 0;
+        bool have = false;
+        if (alive) {
+            have = next_hit(leaf, t0, t1, fidx);
+            if (!have) alive = false;
+        }
+        bool shade = false;
         float af = 0.0f, cx = 0.0f, cy = 0.0f, cz = 0.0f;
         if (have) {
-            fidx = __ldg(p.leaf_flut + leaf);
-            const double sigma = __ldg(p.sigma + fidx);
-            const double delta = t1 - t0;
-            if (kMode == kRender && depth == CUDART_INF && sigma > p.sigma_dep) depth = t0;
-            const double em = exp(-sigma * delta);
-            const double a = T * (1.0 - em);
-            if (a > 0.0) {
-                shade = true;
-                af = (float)a;
-                const double *R = p.rot_inv + 9 * __ldg(p.rot_index + fidx);
-                cx = (float)(R[0] * dw[0] + R[1] * dw[1] + R[2] * dw[2]);
-                cy = (float)(R[3] * dw[0] + R[4] * dw[1] + R[5] * dw[2]);
-                cz = (float)(R[6] * dw[0] + R[7] * dw[1] + R[8] * dw[2]);
-                acc = acc + a;
+            if (kMode == kCount) {
+                ++hits;
+            } else {
+                const double sigma = __ldg(p.sigma + fidx);
+                const double delta = t1 - t0;
+                if (kMode == kRender && depth == CUDART_INF && sigma > p.sigma_dep) depth = t0;
+                const double em = exp(-sigma * delta);
+                const double a = T * (1.0 - em);
+                if (a > 0.0) {
+                    shade = true;
+                    af = (float)a;
+                    const double *R = p.rot_inv + 9 * __ldg(p.rot_index + fidx);
+                    cx = (float)(R[0] * dw[0] + R[1] * dw[1] + R[2] * dw[2]);
+                    cy = (float)(R[3] * dw[0] + R[4] * dw[1] + R[5] * dw[2]);
+                    cz = (float)(R[6] * dw[0] + R[7] * dw[1] + R[8] * dw[2]);
+                    acc = acc + a;
+                }
+                T = T * em;
+                if (kMode == kTrace) {
+                    p.hit_idx[trace_base + hits] = (int64_t)fidx;
+                    p.hit_t0[trace_base + hits] = t0;
+                    p.hit_t1[trace_base + hits] = t1;
+                }
+                ++hits;
+                if (kMode == kRender && p.early_stop && acc > p.stop) alive = false;
             }
-            T = T * em;
-            if (kMode == kTrace) {
-                p.hit_idx[trace_base + hits] = (int64_t)fidx;
-                p.hit_t0[trace_base + hits] = t0;
-                p.hit_t1[trace_base + hits] = t1;
-            }
-            ++hits;
-            if (kMode == kRender && p.early_stop && acc > p.stop) alive = false;
         }
-        unsigned m = __ballot_sync(0xffffffffu, shade);
-        while (m) {
-            const unsigned src = __fns(m, 0, sub + 1);
-            const bool ok = src < 32;
-            const int s = ok ? (int)src : 0;
-            const uint32_t bf = __shfl_sync(0xffffffffu, fidx, s);
-            const float ba = __shfl_sync(0xffffffffu, af, s);
-            const float bx = __shfl_sync(0xffffffffu, cx, s);
-            const float by = __shfl_sync(0xffffffffu, cy, s);
-            const float bz = __shfl_sync(0xffffffffu, cz, s);
-            if (ok) {
-                float Y[H];
-                sh_basis_f<kDeg>(bx, by, bz, Y);
-                const float *row = p.coef + (size_t)bf * p.coef_stride;
-                for (int c = ch0; c < C; c += gs) {
-                    float acc_c = 0.0f;
+        if (kMode != kCount) {
+            unsigned m = __ballot_sync(0xffffffffu, shade);
+            while (m) {
+                const unsigned src = __fns(m, 0, grp + 1);
+                const bool ok = src < 32;
+                const int s = ok ? (int)src : 0;
+                const uint32_t bf = __shfl_sync(0xffffffffu, fidx, s);
+                const float ba = __shfl_sync(0xffffffffu, af, s);
+                const float bx = __shfl_sync(0xffffffffu, cx, s);
+                const float by = __shfl_sync(0xffffffffu, cy, s);
+                const float bz = __shfl_sync(0xffffffffu, cz, s);
+                if (ok) {
+                    float Y[H];
+                    sh_basis_f<kDeg>(bx, by, bz, Y);
+                    if (kVec) {
+                        const float4 *row =
+                            reinterpret_cast<const float4 *>(p.coef + (size_t)bf * p.coef_stride);
+                        float4 *dst = reinterpret_cast<float4 *>(feat + s * cp);
+                        for (int c4 = q; c4 < units; c4 += lph) {
+                            float4 v[H];
 #pragma unroll
-                    for (int h = 0; h < H; ++h) acc_c = fmaf(__ldg(row + h * C + c), Y[h], acc_c);
-                    feat[s * cstride + c] += ba * acc_c;
+                            for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
+                            float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+#pragma unroll
+                            for (int h = 0; h < H; ++h) {
+                                ax = fmaf(v[h].x, Y[h], ax);
+                                ay = fmaf(v[h].y, Y[h], ay);
+                                az = fmaf(v[h].z, Y[h], az);
+                                aw = fmaf(v[h].w, Y[h], aw);
+                            }
+                            float4 f = dst[c4];
+                            f.x += ba * ax;
+                            f.y += ba * ay;
+                            f.z += ba * az;
+                            f.w += ba * aw;
+                            dst[c4] = f;
+                        }
+                    } else {
+                        const float *row = p.coef + (size_t)bf * p.coef_stride;
+                        for (int c = q; c < C; c += lph) {
+                            float acc_c = 0.0f;
+#pragma unroll
+                            for (int h = 0; h < H; ++h)
+                                acc_c = fmaf(__ldg(row + h * C + c), Y[h], acc_c);
+                            feat[s * cp + c] += ba * acc_c;
+                        }
+                    }
+                }
+                for (int k = 0; k < hpi && m; ++k) m &= m - 1;
+            }
+        }
+        // ---- retire finished rays: scalars per lane, features row by row
+        const bool done = ray >= 0 && !alive;
+        if (done) finish_ray();
+        if (kMode != kCount) {
+            unsigned fm = __ballot_sync(0xffffffffu, done && acc > 0.0);
+            __syncwarp();
+            while (fm) {
+                const int s = __ffs(fm) - 1;
+                fm &= fm - 1;
+                const int64_t r = __shfl_sync(0xffffffffu, ray, s);
+                for (int c = lane; c < C; c += 32) {
+                    p.F[r * C + c] = feat[s * cp + c];
+                    feat[s * cp + c] = 0.0f;
                 }
             }
-            for (int k = 0; k < hpr && m; ++k) m &= m - 1;
+            __syncwarp();
+            // a retired ray with acc == 0 never touched its row (rows start at
+            // zero and F was cleared before the launch)
         }
-        if (__ballot_sync(0xffffffffu, alive) == 0) break;
-    }
-
-    if (kMode == kCount) {
-        if (ray >= 0) p.counts[ray] = hits;
-        return;
-    }
-    if (ray >= 0) {
-        if (p.A64) p.A64[ray] = acc;
-        if (p.A32) p.A32[ray] = (float)acc;
-        if (kMode == kRender) {
-            if (p.D64) p.D64[ray] = depth;
-            if (p.D32) p.D32[ray] = (float)depth;
-        }
-    }
-    __syncwarp();
-    // features: one ray at a time, channels across the lanes
-    for (int rl = 0; rl < 32; ++rl) {
-        const int64_t r = __shfl_sync(0xffffffffu, ray, rl);
-        if (r < 0) continue;
-        for (int c = lane; c < C; c += 32) p.F[r * C + c] = feat[rl * cstride + c];
+        if (done) ray = -1;
     }
 }
 
-template <int kMode, bool kCamera>
-int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
-    const int blocks = (int)ceil_div<int64_t>(warps, kRenderWarps);
-    if (blocks == 0) return ARTEMIS_OK;
-    const size_t smem = kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * (a.channels | 1) * 4;
-    if (smem > 48 * 1024) {
-        // opt in to the large carve-out once per instantiation
-        switch (degree) {
-#define ARTEMIS_ATTR(D) case D: cudaFuncSetAttribute(render_kernel<D, kMode, kCamera>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-            ARTEMIS_ATTR(0) ARTEMIS_ATTR(1) ARTEMIS_ATTR(2) ARTEMIS_ATTR(3) ARTEMIS_ATTR(4)
-#undef ARTEMIS_ATTR
-        }
-    }
+template <int kMode, bool kCamera, bool kVec>
+int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
+    if (warps == 0) return ARTEMIS_OK;
+    const int cp = kVec ? a.channels + 4 : (a.channels | 1);
+    const size_t smem = kStackBytes + (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4);
+    const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {
-        case 0: render_kernel<0, kMode, kCamera><<<blocks, kRenderThreads, smem, st>>>(a); break;
-        case 1: render_kernel<1, kMode, kCamera><<<blocks, kRenderThreads, smem, st>>>(a); break;
-        case 2: render_kernel<2, kMode, kCamera><<<blocks, kRenderThreads, smem, st>>>(a); break;
-        case 3: render_kernel<3, kMode, kCamera><<<blocks, kRenderThreads, smem, st>>>(a); break;
-        case 4: render_kernel<4, kMode, kCamera><<<blocks, kRenderThreads, smem, st>>>(a); break;
-        default: return ARTEMIS_ERR_ARG;
+#define ARTEMIS_LAUNCH(D)                                                                       \
+    case D: {                                                                                   \
+        auto kern = render_kernel<D, kMode, kCamera, kVec>;                                     \
+        if (smem > 48 * 1024)                                                                   \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        int occ = 0;                                                                            \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRenderThreads, smem);        \
+        const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * (occ > 0 ? occ : 1)); \
+        kern<<<blocks, kRenderThreads, smem, st>>>(a);                                          \
+        break;                                                                                  \
+    }
+        ARTEMIS_LAUNCH(0) ARTEMIS_LAUNCH(1) ARTEMIS_LAUNCH(2) ARTEMIS_LAUNCH(3) ARTEMIS_LAUNCH(4)
+#undef ARTEMIS_LAUNCH
+        default:
+            return ARTEMIS_ERR_ARG;
     }
     return ARTEMIS_LAUNCHED();
 }
 
+template <int kMode, bool kCamera>
+int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
+    const bool vec = kMode != kCount && a.channels % 4 == 0 && a.coef_stride % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(a.coef) & 15) == 0;
+    return vec ? launch_render_vec<kMode, kCamera, true>(degree, a, warps, st)
+               : launch_render_vec<kMode, kCamera, false>(degree, a, warps, st);
+}
+
 static void fill_tree(RenderArgs &a, const artemis_tree_view *t) {
     a.nodes = static_cast<const PackedNode *>(t->nodes);
-    a.leaf_flut = t->flut_idx;
+    a.leaves = static_cast<const uint4 *>(t->leaves);
     a.n_leaves = t->n_leaves;
     a.n_leaves_dev = t->n_leaves_dev;
 }
@@ -409,12 +541,15 @@ static void fill_rays(RenderArgs &a, const artemis_rays *r) {
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, double lambda_th,
                   double sigma_dep, int early_stop, float *F, float *A, float *D,
-                  cudaStream_t st) {
+                  unsigned long long *queue, cudaStream_t st) {
     RenderArgs a{};
     fill_tree(a, tree);
     fill_shade(a, shade);
     a.cam = cam_dev;
+    a.queue = queue;
+    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)width * height * shade->channels * sizeof(float), st));
     a.tiles_x = (width + 7) / 8;
+    a.tiles_y = (height + 3) / 4;
     a.n_rays = (int64_t)width * height;
     a.t_min = 0.0;
     a.t_max = HUGE_VAL;
@@ -460,8 +595,21 @@ __global__ void flut_split_kernel(const Tin *__restrict__ flut, int64_t n, int w
 
 using namespace artemis;
 
+// Launch helper for the API entry points: a stream-ordered 8-byte ray-queue
+// counter around the launch.
+template <typename Fn>
+static int with_queue(RenderArgs &a, cudaStream_t st, Fn &&launch) {
+    unsigned long long *q = nullptr;
+    ARTEMIS_TRY(cudaMallocAsync(reinterpret_cast<void **>(&q), sizeof(*q), st));
+    ARTEMIS_TRY(cudaMemsetAsync(q, 0, sizeof(*q), st));
+    a.queue = q;
+    int rc = launch();
+    cudaFreeAsync(q, st);
+    return rc;
+}
+
 static bool valid_common(const artemis_tree_view *t, const artemis_rays *r) {
-    return t && r && t->nodes && t->flut_idx && r->n_rays >= 0 &&
+    return t && r && t->nodes && t->leaves && r->n_rays >= 0 &&
            (r->n_rays == 0 || (r->origins_g && r->dirs_g));
 }
 
@@ -482,8 +630,13 @@ extern "C" int artemis_render_rays(const artemis_tree_view *tree, const artemis_
     a.F = F;
     a.A64 = alpha;
     a.D64 = depth;
-    return launch_render_deg<kRender, false>(shade->degree, a, ceil_div<int64_t>(rays->n_rays, 32),
-                                             S(stream));
+    if (rays->n_rays == 0) return ARTEMIS_OK;
+    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)rays->n_rays * shade->channels * sizeof(float),
+                                S(stream)));
+    return with_queue(a, S(stream), [&] {
+        return launch_render_deg<kRender, false>(shade->degree, a,
+                                                 ceil_div<int64_t>(rays->n_rays, 32), S(stream));
+    });
 }
 
 extern "C" int artemis_count_hits(const artemis_tree_view *tree, const artemis_rays *rays,
@@ -494,7 +647,11 @@ extern "C" int artemis_count_hits(const artemis_tree_view *tree, const artemis_r
     fill_rays(a, rays);
     a.channels = 1;
     a.counts = counts;
-    return launch_render_deg<kCount, false>(0, a, ceil_div<int64_t>(rays->n_rays, 32), S(stream));
+    if (rays->n_rays == 0) return ARTEMIS_OK;
+    return with_queue(a, S(stream), [&] {
+        return launch_render_deg<kCount, false>(0, a, ceil_div<int64_t>(rays->n_rays, 32),
+                                                S(stream));
+    });
 }
 
 extern "C" int artemis_forward_fit(const artemis_tree_view *tree, const artemis_shading *shade,
@@ -517,8 +674,13 @@ extern "C" int artemis_forward_fit(const artemis_tree_view *tree, const artemis_
     a.hit_idx = hit_idx;
     a.hit_t0 = hit_t0;
     a.hit_t1 = hit_t1;
-    return launch_render_deg<kTrace, false>(shade->degree, a, ceil_div<int64_t>(rays->n_rays, 32),
-                                            S(stream));
+    if (rays->n_rays == 0) return ARTEMIS_OK;
+    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)rays->n_rays * shade->channels * sizeof(float),
+                                S(stream)));
+    return with_queue(a, S(stream), [&] {
+        return launch_render_deg<kTrace, false>(shade->degree, a,
+                                                ceil_div<int64_t>(rays->n_rays, 32), S(stream));
+    });
 }
 
 extern "C" int artemis_camera_rays(const artemis_camera *cam, double *og, double *dg, double *dw,

@@ -81,12 +81,13 @@ __device__ void build_node(const K *__restrict__ c, int64_t n, int64_t i, int32_
         PackedNode p;
         pack_child(p.w, cf, (u64)c[split], l);
         pack_child(p.w + 4, (u64)c[split + 1], cl, r);
+        p.w[0] |= (uint32_t)split_axis_of(range_free_bits(cf, cl)) << 27;
         reinterpret_cast<uint4 *>(nodes + i)[0] = make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]);
         reinterpret_cast<uint4 *>(nodes + i)[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
         if (i == 0) {
             PackedNode s;
             pack_child(s.w, (u64)c[0], (u64)c[n - 1], 0);
-            s.w[4] = kAbsent << 21;
+            s.w[4] = kAbsent;
             s.w[5] = s.w[6] = 0;
             s.w[7] = 0;
             reinterpret_cast<uint4 *>(nodes + (n - 1))[0] = make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
@@ -100,15 +101,21 @@ template <typename K>
 __global__ void build_tree_kernel(const K *__restrict__ codes, int64_t n_host,
                                   const int32_t *__restrict__ n_dev, int32_t *left, int32_t *right,
                                   int32_t *bmin, int32_t *bsize, PackedNode *nodes,
+                                  uint4 *leaves, const uint32_t *__restrict__ leaf_flut,
                                   int32_t *dup_flag) {
     int64_t n = n_dev ? (int64_t)*n_dev : n_host;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (leaves && i < n) {
+        u64 c = (u64)codes[i];
+        leaves[i] = make_uint4((uint32_t)compact_bits3(c), (uint32_t)compact_bits3(c >> 1),
+                               (uint32_t)compact_bits3(c >> 2), leaf_flut[i]);
+    }
     if (n == 1 && i == 0 && nodes) {
         // single leaf: root = ~0, only the super-root record exists
         PackedNode s;
         u64 c0 = (u64)codes[0];
         pack_child(s.w, c0, c0, ~0);
-        s.w[4] = kAbsent << 21;
+        s.w[4] = kAbsent;
         s.w[5] = s.w[6] = s.w[7] = 0;
         reinterpret_cast<uint4 *>(nodes)[0] = make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
         reinterpret_cast<uint4 *>(nodes)[1] = make_uint4(s.w[4], s.w[5], s.w[6], s.w[7]);
@@ -119,11 +126,18 @@ __global__ void build_tree_kernel(const K *__restrict__ codes, int64_t n_host,
 }
 
 // API path: packed records from the reference arrays (any valid tree).
-__global__ void pack_tree_kernel(const u64 *__restrict__ codes, int64_t n, int32_t root,
+__global__ void pack_tree_kernel(const u64 *__restrict__ codes,
+                                 const uint32_t *__restrict__ flut_idx, int64_t n, int32_t root,
                                  const int32_t *__restrict__ left, const int32_t *__restrict__ right,
                                  const int32_t *__restrict__ bmin,
-                                 const int32_t *__restrict__ bsize, PackedNode *nodes) {
+                                 const int32_t *__restrict__ bsize, PackedNode *nodes,
+                                 uint4 *leaves) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        u64 c = codes[i];
+        leaves[i] = make_uint4((uint32_t)compact_bits3(c), (uint32_t)compact_bits3(c >> 1),
+                               (uint32_t)compact_bits3(c >> 2), flut_idx[i]);
+    }
     auto child = [&](uint32_t *w, int32_t link) {
         if (link < 0) {
             u64 c = codes[~link];
@@ -143,9 +157,12 @@ __global__ void pack_tree_kernel(const u64 *__restrict__ codes, int64_t n, int32
     if (i < n - 1) {
         child(p.w, left[i]);
         child(p.w + 4, right[i]);
+        const int32_t *s = bsize + 3 * i;
+        const int fb = (__ffs(s[0]) - 1) + (__ffs(s[1]) - 1) + (__ffs(s[2]) - 1);
+        p.w[0] |= (uint32_t)split_axis_of(fb) << 27;
     } else if (i == (n > 1 ? n - 1 : 0)) {
         child(p.w, root);
-        p.w[4] = kAbsent << 21;
+        p.w[4] = kAbsent;
         p.w[5] = p.w[6] = p.w[7] = 0;
     } else {
         return;
@@ -157,20 +174,22 @@ __global__ void pack_tree_kernel(const u64 *__restrict__ codes, int64_t n, int32
 template <typename K>
 int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
                       int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
-                      PackedNode *nodes, int32_t *dup_flag, cudaStream_t st) {
-    int64_t threads = n_cap > 1 ? n_cap - 1 : 1;
+                      PackedNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
+                      int32_t *dup_flag, cudaStream_t st) {
+    int64_t threads = n_cap > 1 ? n_cap : 1;
     int blocks = (int)ceil_div<int64_t>(threads, 256);
     build_tree_kernel<K><<<blocks, 256, 0, st>>>(codes, n_host, n_dev, left, right, bmin, bsize,
-                                                  nodes, dup_flag);
+                                                  nodes, leaves, leaf_flut, dup_flag);
     return ARTEMIS_LAUNCHED();
 }
 
 template int launch_build_tree<u64>(const u64 *, int64_t, const int32_t *, int64_t, int32_t *,
-                                    int32_t *, int32_t *, int32_t *, PackedNode *, int32_t *,
-                                    cudaStream_t);
+                                    int32_t *, int32_t *, int32_t *, PackedNode *, uint4 *,
+                                    const uint32_t *, int32_t *, cudaStream_t);
 template int launch_build_tree<uint32_t>(const uint32_t *, int64_t, const int32_t *, int64_t,
                                          int32_t *, int32_t *, int32_t *, int32_t *,
-                                         PackedNode *, int32_t *, cudaStream_t);
+                                         PackedNode *, uint4 *, const uint32_t *, int32_t *,
+                                         cudaStream_t);
 
 }  // namespace artemis
 
@@ -202,17 +221,18 @@ extern "C" int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *lef
     if (n == 1) return ARTEMIS_OK;
     if (!left || !right || !box_min || !box_size) return ARTEMIS_ERR_ARG;
     return launch_build_tree<u64>(reinterpret_cast<const u64 *>(codes), n, nullptr, n, left,
-                                  right, box_min, box_size, nullptr, dup_flag, S(stream));
+                                  right, box_min, box_size, nullptr, nullptr, nullptr, dup_flag,
+                                  S(stream));
 }
 
-extern "C" int artemis_pack_tree(const uint64_t *codes, int64_t n, int32_t root,
-                                 const int32_t *left, const int32_t *right,
+extern "C" int artemis_pack_tree(const uint64_t *codes, const uint32_t *flut_idx, int64_t n,
+                                 int32_t root, const int32_t *left, const int32_t *right,
                                  const int32_t *box_min, const int32_t *box_size, void *nodes,
-                                 artemis_stream stream) {
-    if (n < 1 || !codes || !nodes) return ARTEMIS_ERR_ARG;
+                                 void *leaves, artemis_stream stream) {
+    if (n < 1 || !codes || !flut_idx || !nodes || !leaves) return ARTEMIS_ERR_ARG;
     if (n > 1 && (!left || !right || !box_min || !box_size)) return ARTEMIS_ERR_ARG;
     pack_tree_kernel<<<(int)ceil_div<int64_t>(n, 256), 256, 0, S(stream)>>>(
-        reinterpret_cast<const u64 *>(codes), n, root, left, right, box_min, box_size,
-        reinterpret_cast<PackedNode *>(nodes));
+        reinterpret_cast<const u64 *>(codes), flut_idx, n, root, left, right, box_min, box_size,
+        reinterpret_cast<PackedNode *>(nodes), reinterpret_cast<uint4 *>(leaves));
     return ARTEMIS_LAUNCHED();
 }

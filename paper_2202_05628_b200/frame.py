@@ -136,6 +136,9 @@ class FramePipeline:
                                   rot.ctypes.data if rot is not None else None, nj, C.byref(cam),
                                   float(lambda_th), float(sigma_dep), flags, ptr(F), ptr(A),
                                   ptr(D), self.stream.cuda_stream or None), "frame_run")
+        cur = torch.cuda.current_stream()
+        if cur != self.stream:
+            cur.wait_stream(self.stream)  # consumers on the caller's stream see the frame
         return F, A, D
 
     def counts(self):

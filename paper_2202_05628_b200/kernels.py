@@ -131,10 +131,11 @@ class DeviceTree:
         else:
             self.left = self.right = self.bmin = self.bsize = None
         self.nodes = workspace(32 * n)
-        check(L.artemis_pack_tree(ptr(self.codes), n, int(root), ptr(self.left), ptr(self.right),
-                                  ptr(self.bmin), ptr(self.bsize), ptr(self.nodes),
-                                  stream_handle()), "pack_tree")
-        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.flut_idx), n, None)
+        self.leaves = workspace(16 * n)
+        check(L.artemis_pack_tree(ptr(self.codes), ptr(self.flut_idx), n, int(root),
+                                  ptr(self.left), ptr(self.right), ptr(self.bmin), ptr(self.bsize),
+                                  ptr(self.nodes), ptr(self.leaves), stream_handle()), "pack_tree")
+        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.leaves), n, None)
 
 
 class DeviceShading:
