@@ -110,6 +110,9 @@ typedef struct {
     const void *leaves;         /* artemis_pack_tree output: leaf records */
     int64_t n_leaves;           /* host value; ignored when n_leaves_dev != NULL */
     const int32_t *n_leaves_dev;/* device count (device pipeline), may be NULL */
+    double coord_max;           /* bound on every box coordinate (the grid
+                                   resolution); 0 = 2^21. Only tunes the fp32
+                                   filter; results never depend on it. */
 } artemis_tree_view;
 
 typedef struct {

@@ -28,7 +28,8 @@ OK, ERR_ARG, ERR_RANGE, ERR_EMPTY, ERR_DUP, ERR_OOM, ERR_CUDA, ERR_WS, ERR_NODEV
 
 
 class TreeView(C.Structure):
-    _fields_ = [("nodes", P), ("leaves", P), ("n_leaves", I64), ("n_leaves_dev", P)]
+    _fields_ = [("nodes", P), ("leaves", P), ("n_leaves", I64), ("n_leaves_dev", P),
+                ("coord_max", DBL)]
 
 
 class Shading(C.Structure):

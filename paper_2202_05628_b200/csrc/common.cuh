@@ -70,10 +70,11 @@ __host__ __device__ __forceinline__ u64 morton3(u64 x, u64 y, u64 z) {
 // One internal node = 32 bytes: both children's octant boxes (min corner
 // plus the number of free Morton bits, which fixes the per-axis power-of-two
 // size exactly as _core.pyx:182-190 does) and the child links.
-// word[0] = L.x | L.free << 21 | split_axis << 27, word[1] = L.y,
-// word[2] = L.z, word[3] = left
-// word[4] = R.x | R.free << 21 | absent << 31, word[5] = R.y, word[6] = R.z,
-// word[7] = right
+// word[0] = L.x | L.sx << 21 | split_axis << 27, word[1] = L.y | L.sy << 21,
+// word[2] = L.z | L.sz << 21, word[3] = left
+// word[4] = R.x | R.sx << 21 | absent << 31, word[5] = R.y | R.sy << 21,
+// word[6] = R.z | R.sz << 21, word[7] = right
+// with s_a = log2 of the box size on axis a (box_size_axis of the free bits).
 // split_axis is the axis of the node's highest differing Morton bit: the
 // plane that separates the two children's octants. kAbsent marks a missing
 // child (the super-root's right).
@@ -97,12 +98,23 @@ __device__ __forceinline__ int range_free_bits(u64 a, u64 b) {
     return a == b ? 0 : 64 - __clzll(static_cast<long long>(a ^ b));
 }
 
+__host__ __device__ __forceinline__ int log_size_axis(int free_bits, int axis) {
+    return (free_bits + 2 - axis) / 3;
+}
+
+__device__ __forceinline__ void pack_box(uint32_t *w, uint32_t x, uint32_t y, uint32_t z,
+                                         int free_bits) {
+    w[0] = x | ((uint32_t)log_size_axis(free_bits, 0) << 21);
+    w[1] = y | ((uint32_t)log_size_axis(free_bits, 1) << 21);
+    w[2] = z | ((uint32_t)log_size_axis(free_bits, 2) << 21);
+}
+
 __device__ __forceinline__ void pack_child(uint32_t *w, u64 c_first, u64 c_last, int link) {
     int fb = range_free_bits(c_first, c_last);
     u64 base = fb >= 64 ? 0ull : (c_first >> fb) << fb;
-    w[0] = static_cast<uint32_t>(compact_bits3(base)) | (static_cast<uint32_t>(fb) << 21);
-    w[1] = static_cast<uint32_t>(compact_bits3(base >> 1));
-    w[2] = static_cast<uint32_t>(compact_bits3(base >> 2));
+    pack_box(w, static_cast<uint32_t>(compact_bits3(base)),
+             static_cast<uint32_t>(compact_bits3(base >> 1)),
+             static_cast<uint32_t>(compact_bits3(base >> 2)), fb);
     w[3] = static_cast<uint32_t>(link);
 }
 

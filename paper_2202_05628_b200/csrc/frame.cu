@@ -133,7 +133,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     mark(4);
     const int passes = f->key_bits <= 0 ? 1 : (f->key_bits + 7) / 8;
     launches += 2 + passes + 3 + 1;
-    artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1};
+    artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, lambda_th, sigma_dep,

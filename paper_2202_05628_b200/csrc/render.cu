@@ -36,6 +36,12 @@ constexpr int kRenderThreads = 32 * kRenderWarps;
 constexpr int kSmemStack = 32;       // per-thread stack entries kept in shared memory
 constexpr int kStack = 68;           // tree depth <= 64 key bits + super-root; overflow in local
 constexpr int kStackBytes = kSmemStack * kRenderThreads * 4;
+constexpr int kQCap = 8;             // leaves queued per lane per round
+constexpr int kQThresh = 64;         // warp-wide queued leaves that end a traversal phase
+constexpr int kMaxSteps = 64;        // traversal steps per phase at most
+// per queued leaf: leaf id / FLUT row (4) + t0 (8) + exp(-sigma*delta) (8) + (a, dir) (16)
+constexpr int kQueueBytes = kQCap * kRenderThreads * (4 + 8 + 8 + 16);
+constexpr uint32_t kDenseFlag = 1u << 31;  // queued row's density exceeds sigma_dep
 constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~leaf)
 }  // namespace
 
@@ -61,6 +67,7 @@ struct RenderArgs {
     unsigned long long *queue;  // ray-id counter, zero at launch
     double t_min, t_max;
     double stop;  // 1 - lambda_th
+    float coord_max;  // upper bound of every box coordinate (grid resolution)
     double sigma_dep;
     int early_stop;
     // outputs
@@ -78,13 +85,13 @@ struct RenderArgs {
 __device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2,
                                            const double o[3], const double d[3], double t_min,
                                            double t_max, double &t0o, double &t1o) {
-    const int fb = (int)((w0 >> 21) & 63u);
-    const int lo_i[3] = {(int)(w0 & kCoordMask), (int)(w1 & kCoordMask), (int)(w2 & kCoordMask)};
+    const uint32_t w[3] = {w0, w1, w2};
     double t0 = t_min, t1 = t_max;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double lo = (double)lo_i[a];
-        const double hi = (double)(lo_i[a] + box_size_axis(fb, a));
+        const int lo_i = (int)(w[a] & kCoordMask);
+        const double lo = (double)lo_i;
+        const double hi = (double)(lo_i + (1 << ((w[a] >> 21) & 31u)));
         if (d[a] == 0.0) {
             if (o[a] < lo || o[a] >= hi) return false;
         } else {
@@ -105,33 +112,52 @@ __device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2
     return true;
 }
 
-// Filtered hit test: the slab planes are scaled by a per-ray reciprocal
-// instead of divided, which is within 3 ulp of the exact quotient; the
-// decision t0 < t1 is taken from it only when the gap exceeds a bound far
-// above that error (2^-50 relative), otherwise the exact test decides. So
-// the answer always equals clip_exact's; only its cost differs.
+// Per-ray constants of the fp32 filtered box test.
+struct RayF {
+    float o_inv[3], inv[3];  // o * (1/d) and 1/d in fp32 (axes with d != 0)
+    float c[3];              // |o * (1/d)|: the cancellation scale of each axis
+    float tmin_up, tmin_dn, tmax_up, tmax_dn;
+    bool exact_only;         // some d == 0: every test takes the exact path
+};
+
+__device__ __forceinline__ float int_to_float_exact(uint32_t v) {
+    // v < 2^23: place v in the mantissa of 2^23 and subtract (exact, 2 ops)
+    return __int_as_float(0x4B000000 | v) - 8388608.0f;
+}
+
+// Filtered hit test. A plane distance t = (lo - o)/d is evaluated in fp32 as
+// fma(lo, 1/d, -o/d); with 1/d and o/d rounded to fp32 its error is at most
+// 2^-23 (|o/d| + |t|). The entry maximum e and exit minimum x carry the
+// |o/d| of the axis that produced them, and t0 < t1 is decided from (e, x)
+// only when the gap exceeds 4x their combined error bound; otherwise the
+// exact fp64 slab test decides. The answer always equals clip_exact's.
 __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t w2,
-                                             const double o[3], const double d[3],
-                                             const double inv[3], double t_min, double t_max) {
-    const int fb = (int)((w0 >> 21) & 63u);
-    const int lo_i[3] = {(int)(w0 & kCoordMask), (int)(w1 & kCoordMask), (int)(w2 & kCoordMask)};
-    double t0 = t_min, t1 = t_max;
+                                             const RayF &rf, const double o[3],
+                                             const double d[3], double t_min, double t_max) {
+    if (!rf.exact_only) {
+        const uint32_t w[3] = {w0, w1, w2};
+        float e = -INFINITY, x = INFINITY, ec = 0.0f, xc = 0.0f;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const double lo = (double)lo_i[a];
-        const double hi = (double)(lo_i[a] + box_size_axis(fb, a));
-        if (d[a] == 0.0) {
-            if (o[a] < lo || o[a] >= hi) return false;
-        } else {
-            double ta = (lo - o[a]) * inv[a];
-            double tb = (hi - o[a]) * inv[a];
-            t0 = fmax(t0, fmin(ta, tb));
-            t1 = fmin(t1, fmax(ta, tb));
+        for (int a = 0; a < 3; ++a) {
+            const uint32_t lo_i = w[a] & kCoordMask;
+            const float lo = int_to_float_exact(lo_i);
+            const float hi = int_to_float_exact(lo_i + (1u << ((w[a] >> 21) & 31u)));
+            const float ta = fmaf(lo, rf.inv[a], -rf.o_inv[a]);
+            const float tb = fmaf(hi, rf.inv[a], -rf.o_inv[a]);
+            const float en = fminf(ta, tb), ex = fmaxf(ta, tb);
+            if (en > e) {
+                e = en;
+                ec = rf.c[a];
+            }
+            if (ex < x) {
+                x = ex;
+                xc = rf.c[a];
+            }
         }
+        const float m = 4.76837158203125e-07f * (fabsf(e) + fabsf(x) + ec + xc);  // 2^-21
+        if (e + m < x && e + m < rf.tmax_dn && rf.tmin_up + m < x) return true;
+        if (e > x + m || e > rf.tmax_up + m || rf.tmin_dn > x + m) return false;
     }
-    const double m = 8.881784197001252e-16 * (fabs(t0) + (isinf(t1) ? 0.0 : fabs(t1)));
-    if (t0 + m < t1) return true;
-    if (t0 > t1 + m) return false;
     double e0, e1;
     return clip_exact(w0, w1, w2, o, d, t_min, t_max, e0, e1);
 }
@@ -194,40 +220,58 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
 }
 
 // Persistent warps pull rays from a global queue (ids in 8x4 pixel-tile order
-// in camera mode) and refill idle lanes as rays finish, so SIMD lanes stay
-// busy despite the ~6x spread of per-ray work. Each lane walks its ray's
-// DFS with a stack in shared memory (column per thread, so lanes at
-// different depths never bank-conflict). Child visiting order uses the
-// split axis: the two children's octants are separated by the plane of the
-// node's highest differing Morton bit, so when both are hit the one on the
-// ray's side of that plane has the smaller entry distance -- the order the
-// reference's `lt0 <= rt0` comparison yields (_core.pyx:345), without
-// computing either distance. Internal-node tests use the filtered predicate;
-// emitted leaves get exact fp64 intervals. Visible hits of a round are then
-// shaded by lane groups.
+// in camera mode) and refill idle lanes as rays finish. Each round runs
+// three warp-uniform phases instead of one divergent per-ray loop:
+//  A. traversal: every lane takes one DFS step per iteration (expand one
+//     node, or queue one leaf) until the warp has kQThresh leaves queued.
+//     A queued leaf is already known to be hit: near children are tested
+//     when their parent is expanded, far children before they are pushed.
+//  B. integration: the queued leaves are processed cooperatively (exact
+//     fp64 slab interval, density, exp(-sigma delta), canonical direction);
+//     then each lane runs the cheap sequential part of the reference's
+//     per-ray loop over its own leaves in order -- transmittance, alpha,
+//     depth, early stop (_core.pyx:534-556). Leaves queued past an early
+//     stop are dropped.
+//  C. shading: lane groups of C/4 lanes read one FLUT row as float4
+//     segments per visible leaf, slot by slot so each ray's features
+//     accumulate in ray order.
+// The DFS stack lives in shared memory (a column per thread). Child order
+// uses the split axis: the children's octants are separated by the plane of
+// the node's highest differing Morton bit, so when both are hit the one on
+// the ray's side of that plane has the smaller entry distance -- the order
+// the reference's `lt0 <= rt0` comparison yields (_core.pyx:345). Internal
+// tests use the fp32 filter; emitted leaves get exact fp64 intervals.
 template <int kDeg, int kMode, bool kCamera, bool kVec>
 __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
+    unsigned char *qbase = s_raw + kStackBytes;
+    uint32_t *q_id = reinterpret_cast<uint32_t *>(qbase);                            // leaf, then row
+    double *q_t0 = reinterpret_cast<double *>(qbase + kQCap * kRenderThreads * 4);
+    double *q_em = reinterpret_cast<double *>(qbase + kQCap * kRenderThreads * 12);
+    float4 *q_val = reinterpret_cast<float4 *>(qbase + kQCap * kRenderThreads * 20);  // a, dir
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
     const int cp = kVec ? C + 4 : (C | 1);
-    float *feat = reinterpret_cast<float *>(s_raw + kStackBytes) + (size_t)warp * 32 * cp;
+    float *feat = reinterpret_cast<float *>(s_raw + kStackBytes + kQueueBytes) +
+                  (size_t)warp * 32 * cp;
     if (kMode != kCount)
         for (int i = lane; i < 32 * cp; i += 32) feat[i] = 0.0f;
     const int64_t n_leaves = p.n_leaves_dev ? (int64_t)*p.n_leaves_dev : p.n_leaves;
     const int super_root = (int)(n_leaves > 1 ? n_leaves - 1 : 0);
     const int64_t n_ids = kCamera ? (int64_t)p.tiles_x * p.tiles_y * 32 : p.n_rays;
     const unsigned lt = lanemask_lt();
+    const int wbase = warp * 32;  // this warp's column block in the queue arrays
 
     // per-lane ray state
     int64_t ray = -1;
-    bool alive = false;
-    double og[3], dg[3], dw[3], inv[3];
+    bool walking = false;  // DFS not exhausted
+    double og[3], dg[3], dw[3];
+    RayF rf;
     double T = 1.0, acc = 0.0, depth = CUDART_INF;
     int64_t hits = 0, trace_base = 0;
-    int cur = kEnd, top = 0;
+    int cur = kEnd, top = 0, nq = 0;
     int ovf[kStack - kSmemStack];
     bool queue_open = true;
 
@@ -243,57 +287,45 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
         --top;
         return top < kSmemStack ? s_stack[top * kRenderThreads + tid] : ovf[top - kSmemStack];
     };
-    // next occupied leaf front to back (_core.pyx:307-355 order)
-    auto next_hit = [&](int &leaf, double &t0, double &t1, uint32_t &fidx) -> bool {
-        while (cur != kEnd) {
-            if (cur >= 0) {
-                const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur));
-                const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur) + 1);
-                const bool hl = hit_filtered(a.x, a.y, a.z, og, dg, inv, p.t_min, p.t_max);
-                const bool hr = !(b.x & kAbsent) &&
-                                hit_filtered(b.x, b.y, b.z, og, dg, inv, p.t_min, p.t_max);
-                int nxt;
-                uint4 nb;
-                if (hl && hr) {
-                    const bool left_first = dg[(a.x >> 27) & 3u] > 0.0;
-                    push(left_first ? (int)b.w : (int)a.w);
-                    nb = left_first ? a : b;
-                } else if (hl) {
-                    nb = a;
-                } else if (hr) {
-                    nb = b;
-                } else {
-                    cur = pop();
-                    continue;
-                }
-                nxt = (int)nb.w;
-                if (nxt >= 0) {
-                    cur = nxt;  // internal nodes were just tested: expand directly
-                    continue;
-                }
-                cur = pop();
-                double e0, e1;
-                if (clip_exact(nb.x, nb.y, nb.z, og, dg, p.t_min, p.t_max, e0, e1) && e1 > e0) {
-                    leaf = ~nxt;
-                    t0 = e0;
-                    t1 = e1;
-                    fidx = __ldg(&p.leaves[leaf].w);
-                    return true;
-                }
-                continue;
-            }
-            leaf = ~cur;
-            const uint4 L = __ldg(p.leaves + leaf);
-            cur = pop();
-            double e0, e1;
-            if (clip_exact(L.x, L.y, L.z, og, dg, p.t_min, p.t_max, e0, e1) && e1 > e0) {
-                t0 = e0;
-                t1 = e1;
-                fidx = L.w;
-                return true;
-            }
+    auto enqueue = [&](int leaf) {
+        q_id[nq * kRenderThreads + tid] = (uint32_t)leaf;
+        ++nq;
+    };
+    // one DFS step (_core.pyx:307-355 order)
+    auto step = [&]() {
+        if (cur == kEnd) {
+            walking = false;
+            return;
         }
-        return false;
+        if (cur < 0) {  // a far leaf, hit-tested before it was pushed
+            enqueue(~cur);
+            cur = pop();
+            return;
+        }
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur));
+        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur) + 1);
+        const bool hl = hit_filtered(a.x, a.y, a.z, rf, og, dg, p.t_min, p.t_max);
+        const bool hr =
+            !(b.x & kAbsent) && hit_filtered(b.x, b.y, b.z, rf, og, dg, p.t_min, p.t_max);
+        int nxt;
+        if (hl && hr) {
+            const bool left_first = dg[(a.x >> 27) & 3u] > 0.0;
+            push(left_first ? (int)b.w : (int)a.w);
+            nxt = left_first ? (int)a.w : (int)b.w;
+        } else if (hl) {
+            nxt = (int)a.w;
+        } else if (hr) {
+            nxt = (int)b.w;
+        } else {
+            cur = pop();
+            return;
+        }
+        if (nxt >= 0) {
+            cur = nxt;
+        } else {
+            enqueue(~nxt);
+            cur = pop();
+        }
     };
     auto start_ray = [&](int64_t id) {
         ray = -1;
@@ -317,28 +349,32 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
             }
         }
         if (ray < 0) return;
+        rf.exact_only = false;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) inv[a] = dg[a] != 0.0 ? 1.0 / dg[a] : 0.0;
+        for (int a = 0; a < 3; ++a) {
+            if (dg[a] == 0.0) {
+                rf.exact_only = true;
+                rf.inv[a] = rf.o_inv[a] = rf.c[a] = 0.0f;
+            } else {
+                const double inv = 1.0 / dg[a];
+                rf.inv[a] = (float)inv;
+                rf.o_inv[a] = (float)(og[a] * inv);
+                rf.c[a] = fabsf(rf.o_inv[a]);
+            }
+        }
+        rf.tmin_up = __double2float_ru(p.t_min);
+        rf.tmin_dn = __double2float_rd(p.t_min);
+        rf.tmax_up = __double2float_ru(p.t_max);
+        rf.tmax_dn = __double2float_rd(p.t_max);
         T = 1.0;
         acc = 0.0;
         depth = CUDART_INF;
         hits = 0;
         top = 0;
+        nq = 0;
         trace_base = (kMode == kTrace) ? p.offsets[ray] : 0;
-        cur = n_leaves > 0 ? super_root : kEnd;
-        alive = true;
-    };
-    auto finish_ray = [&]() {
-        if (kMode == kCount) {
-            p.counts[ray] = hits;
-        } else {
-            if (p.A64) p.A64[ray] = acc;
-            if (p.A32) p.A32[ray] = (float)acc;
-            if (kMode == kRender) {
-                if (p.D64) p.D64[ray] = depth;
-                if (p.D32) p.D32[ray] = (float)depth;
-            }
-        }
+        cur = (n_leaves > 0 && p.t_min < p.t_max) ? super_root : kEnd;
+        walking = true;
     };
 
     // cooperative shading geometry: lph lanes per hit, hpi hits per pass
@@ -365,99 +401,155 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
             if (!queue_open) break;
             continue;
         }
-        // ---- one traversal step per live lane
-        int leaf = 0;
-        double t0 = 0.0, t1 = 0.0;
-        uint32_t fidx = 0;
-        bool have = false;
-        if (alive) {
-            have = next_hit(leaf, t0, t1, fidx);
-            if (!have) alive = false;
+        // ---- phase A: uniform DFS steps until enough leaves are queued
+        for (int it = 0; it < kMaxSteps; ++it) {
+            const bool can = walking && nq < kQCap;
+            if (__ballot_sync(0xffffffffu, can) == 0) break;
+            if (can) step();
+            if (__reduce_add_sync(0xffffffffu, (unsigned)nq) >= (unsigned)kQThresh) break;
         }
-        bool shade = false;
-        float af = 0.0f, cx = 0.0f, cy = 0.0f, cz = 0.0f;
-        if (have) {
+        // ---- phase B1: exact intervals and per-leaf terms, warp-cooperative
+        __syncwarp();
+        for (int k = 0; k < kQCap; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, nq > k);
+            if (!m) break;
+            const unsigned src = __fns(m, 0, lane + 1);  // lane j takes level k's j-th leaf
+            const int sl = src < 32 ? (int)src : lane;
+            double so[3], sd[3], sw[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                so[a] = __shfl_sync(0xffffffffu, og[a], sl);
+                sd[a] = __shfl_sync(0xffffffffu, dg[a], sl);
+                if (kMode != kCount) sw[a] = __shfl_sync(0xffffffffu, dw[a], sl);
+            }
+            if (src < 32) {
+                const int qi = k * kRenderThreads + wbase + (int)src;
+                const uint4 L = __ldg(p.leaves + q_id[qi]);
+                if (kMode == kCount) continue;
+                double t0 = 0.0, t1 = 0.0;
+                clip_exact(L.x, L.y, L.z, so, sd, p.t_min, p.t_max, t0, t1);
+                const uint32_t fidx = L.w;
+                const double sigma = __ldg(p.sigma + fidx);
+                q_id[qi] = fidx | (sigma > p.sigma_dep ? kDenseFlag : 0u);
+                q_t0[qi] = t0;
+                // trace mode keeps t1 for B2, which writes the CSR trace
+                q_em[qi] = kMode == kTrace ? t1 : exp(-sigma * (t1 - t0));
+                const double *R = p.rot_inv + 9 * __ldg(p.rot_index + fidx);
+                float4 v;
+                v.x = 0.0f;
+                v.y = (float)(R[0] * sw[0] + R[1] * sw[1] + R[2] * sw[2]);
+                v.z = (float)(R[3] * sw[0] + R[4] * sw[1] + R[5] * sw[2]);
+                v.w = (float)(R[6] * sw[0] + R[7] * sw[1] + R[8] * sw[2]);
+                q_val[qi] = v;
+            }
+        }
+        __syncwarp();
+        // ---- phase B2: sequential per-ray integration over own leaves
+        for (int k = 0; k < nq; ++k) {
+            const int qi = k * kRenderThreads + tid;
+            const uint32_t id = q_id[qi];
             if (kMode == kCount) {
                 ++hits;
+                continue;
+            }
+            const uint32_t fidx = id & ~kDenseFlag;
+            const double t0 = q_t0[qi];
+            double em;
+            if (kMode == kTrace) {
+                const double t1 = q_em[qi];
+                p.hit_idx[trace_base + hits] = (int64_t)fidx;
+                p.hit_t0[trace_base + hits] = t0;
+                p.hit_t1[trace_base + hits] = t1;
+                em = exp(-__ldg(p.sigma + fidx) * (t1 - t0));
             } else {
-                const double sigma = __ldg(p.sigma + fidx);
-                const double delta = t1 - t0;
-                if (kMode == kRender && depth == CUDART_INF && sigma > p.sigma_dep) depth = t0;
-                const double em = exp(-sigma * delta);
-                const double a = T * (1.0 - em);
-                if (a > 0.0) {
-                    shade = true;
-                    af = (float)a;
-                    const double *R = p.rot_inv + 9 * __ldg(p.rot_index + fidx);
-                    cx = (float)(R[0] * dw[0] + R[1] * dw[1] + R[2] * dw[2]);
-                    cy = (float)(R[3] * dw[0] + R[4] * dw[1] + R[5] * dw[2]);
-                    cz = (float)(R[6] * dw[0] + R[7] * dw[1] + R[8] * dw[2]);
-                    acc = acc + a;
-                }
-                T = T * em;
-                if (kMode == kTrace) {
-                    p.hit_idx[trace_base + hits] = (int64_t)fidx;
-                    p.hit_t0[trace_base + hits] = t0;
-                    p.hit_t1[trace_base + hits] = t1;
-                }
-                ++hits;
-                if (kMode == kRender && p.early_stop && acc > p.stop) alive = false;
+                em = q_em[qi];
+            }
+            if (kMode == kRender && depth == CUDART_INF && (id & kDenseFlag)) depth = t0;
+            const double a = T * (1.0 - em);
+            float4 v = q_val[qi];
+            v.x = 0.0f;
+            if (a > 0.0) {
+                v.x = (float)a;
+                acc = acc + a;
+            }
+            q_val[qi] = v;
+            T = T * em;
+            ++hits;
+            if (kMode == kRender && p.early_stop && acc > p.stop) {
+                nq = k + 1;  // drop leaves queued past the stop
+                walking = false;
+                cur = kEnd;
+                break;
             }
         }
+        // ---- phase C: shade the visible queued leaves, slot by slot
         if (kMode != kCount) {
-            unsigned m = __ballot_sync(0xffffffffu, shade);
-            while (m) {
-                const unsigned src = __fns(m, 0, grp + 1);
-                const bool ok = src < 32;
-                const int s = ok ? (int)src : 0;
-                const uint32_t bf = __shfl_sync(0xffffffffu, fidx, s);
-                const float ba = __shfl_sync(0xffffffffu, af, s);
-                const float bx = __shfl_sync(0xffffffffu, cx, s);
-                const float by = __shfl_sync(0xffffffffu, cy, s);
-                const float bz = __shfl_sync(0xffffffffu, cz, s);
-                if (ok) {
-                    float Y[H];
-                    sh_basis_f<kDeg>(bx, by, bz, Y);
-                    if (kVec) {
-                        const float4 *row =
-                            reinterpret_cast<const float4 *>(p.coef + (size_t)bf * p.coef_stride);
-                        float4 *dst = reinterpret_cast<float4 *>(feat + s * cp);
-                        for (int c4 = q; c4 < units; c4 += lph) {
-                            float4 v[H];
+            __syncwarp();
+            for (int k = 0; k < kQCap; ++k) {
+                unsigned m = __ballot_sync(0xffffffffu, nq > k && q_val[k * kRenderThreads + tid].x > 0.0f);
+                if (!__any_sync(0xffffffffu, nq > k)) break;
+                while (m) {
+                    const unsigned src = __fns(m, 0, grp + 1);
+                    if (src < 32) {
+                        const int s = (int)src;
+                        const int qi = k * kRenderThreads + wbase + s;
+                        const uint32_t bf = q_id[qi] & ~kDenseFlag;
+                        const float4 bv = q_val[qi];
+                        float Y[H];
+                        sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
+                        if (kVec) {
+                            const float4 *row = reinterpret_cast<const float4 *>(
+                                p.coef + (size_t)bf * p.coef_stride);
+                            float4 *dst = reinterpret_cast<float4 *>(feat + s * cp);
+                            for (int c4 = q; c4 < units; c4 += lph) {
+                                float4 v[H];
 #pragma unroll
-                            for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
-                            float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+                                for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
+                                float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
 #pragma unroll
-                            for (int h = 0; h < H; ++h) {
-                                ax = fmaf(v[h].x, Y[h], ax);
-                                ay = fmaf(v[h].y, Y[h], ay);
-                                az = fmaf(v[h].z, Y[h], az);
-                                aw = fmaf(v[h].w, Y[h], aw);
+                                for (int h = 0; h < H; ++h) {
+                                    ax = fmaf(v[h].x, Y[h], ax);
+                                    ay = fmaf(v[h].y, Y[h], ay);
+                                    az = fmaf(v[h].z, Y[h], az);
+                                    aw = fmaf(v[h].w, Y[h], aw);
+                                }
+                                float4 f = dst[c4];
+                                f.x += bv.x * ax;
+                                f.y += bv.x * ay;
+                                f.z += bv.x * az;
+                                f.w += bv.x * aw;
+                                dst[c4] = f;
                             }
-                            float4 f = dst[c4];
-                            f.x += ba * ax;
-                            f.y += ba * ay;
-                            f.z += ba * az;
-                            f.w += ba * aw;
-                            dst[c4] = f;
-                        }
-                    } else {
-                        const float *row = p.coef + (size_t)bf * p.coef_stride;
-                        for (int c = q; c < C; c += lph) {
-                            float acc_c = 0.0f;
+                        } else {
+                            const float *row = p.coef + (size_t)bf * p.coef_stride;
+                            for (int c = q; c < C; c += lph) {
+                                float acc_c = 0.0f;
 #pragma unroll
-                            for (int h = 0; h < H; ++h)
-                                acc_c = fmaf(__ldg(row + h * C + c), Y[h], acc_c);
-                            feat[s * cp + c] += ba * acc_c;
+                                for (int h = 0; h < H; ++h)
+                                    acc_c = fmaf(__ldg(row + h * C + c), Y[h], acc_c);
+                                feat[s * cp + c] += bv.x * acc_c;
+                            }
                         }
                     }
+                    for (int j = 0; j < hpi && m; ++j) m &= m - 1;
                 }
-                for (int k = 0; k < hpi && m; ++k) m &= m - 1;
             }
         }
+        nq = 0;
         // ---- retire finished rays: scalars per lane, features row by row
-        const bool done = ray >= 0 && !alive;
-        if (done) finish_ray();
+        const bool done = ray >= 0 && !walking;
+        if (done) {
+            if (kMode == kCount) {
+                p.counts[ray] = hits;
+            } else {
+                if (p.A64) p.A64[ray] = acc;
+                if (p.A32) p.A32[ray] = (float)acc;
+                if (kMode == kRender) {
+                    if (p.D64) p.D64[ray] = depth;
+                    if (p.D32) p.D32[ray] = (float)depth;
+                }
+            }
+        }
         if (kMode != kCount) {
             unsigned fm = __ballot_sync(0xffffffffu, done && acc > 0.0);
             __syncwarp();
@@ -471,8 +563,6 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
                 }
             }
             __syncwarp();
-            // a retired ray with acc == 0 never touched its row (rows start at
-            // zero and F was cleared before the launch)
         }
         if (done) ray = -1;
     }
@@ -482,7 +572,8 @@ template <int kMode, bool kCamera, bool kVec>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels + 4 : (a.channels | 1);
-    const size_t smem = kStackBytes + (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4);
+    const size_t smem = kStackBytes + kQueueBytes +
+                        (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4);
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
@@ -517,6 +608,7 @@ static void fill_tree(RenderArgs &a, const artemis_tree_view *t) {
     a.leaves = static_cast<const uint4 *>(t->leaves);
     a.n_leaves = t->n_leaves;
     a.n_leaves_dev = t->n_leaves_dev;
+    a.coord_max = t->coord_max > 0.0 ? (float)t->coord_max : 2097152.0f;
 }
 
 static void fill_shade(RenderArgs &a, const artemis_shading *s) {

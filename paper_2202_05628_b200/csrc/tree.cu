@@ -146,10 +146,9 @@ __global__ void pack_tree_kernel(const u64 *__restrict__ codes,
             w[2] = (uint32_t)compact_bits3(c >> 2);
         } else {
             const int32_t *m = bmin + 3 * link, *s = bsize + 3 * link;
-            int fb = (__ffs(s[0]) - 1) + (__ffs(s[1]) - 1) + (__ffs(s[2]) - 1);
-            w[0] = (uint32_t)m[0] | ((uint32_t)fb << 21);
-            w[1] = (uint32_t)m[1];
-            w[2] = (uint32_t)m[2];
+            w[0] = (uint32_t)m[0] | ((uint32_t)(__ffs(s[0]) - 1) << 21);
+            w[1] = (uint32_t)m[1] | ((uint32_t)(__ffs(s[1]) - 1) << 21);
+            w[2] = (uint32_t)m[2] | ((uint32_t)(__ffs(s[2]) - 1) << 21);
         }
         w[3] = (uint32_t)link;
     };

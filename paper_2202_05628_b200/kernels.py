@@ -111,6 +111,16 @@ def build_tree(codes, nthreads=1):
     return 0, download(left), download(right), download(bmin), download(bsize)
 
 
+def morton_decode_host(codes) -> np.ndarray:
+    """Host decode of a few codes (no device needed)."""
+    out = np.zeros((len(codes), 3), dtype=np.int64)
+    for i, c in enumerate(np.asarray(codes, dtype=np.uint64)):
+        c = int(c)
+        for a in range(3):
+            out[i, a] = sum(((c >> (3 * b + a)) & 1) << b for b in range(21))
+    return out
+
+
 class DeviceTree:
     """A reference-layout tree on the device plus its packed traversal copy."""
 
@@ -135,7 +145,14 @@ class DeviceTree:
         check(L.artemis_pack_tree(ptr(self.codes), ptr(self.flut_idx), n, int(root),
                                   ptr(self.left), ptr(self.right), ptr(self.bmin), ptr(self.bsize),
                                   ptr(self.nodes), ptr(self.leaves), stream_handle()), "pack_tree")
-        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.leaves), n, None)
+        if n > 1:
+            bm = np.asarray(box_min).reshape(-1, 3)
+            bs = np.asarray(box_size).reshape(-1, 3)
+            r = int(root) if int(root) >= 0 else 0
+            cmax = float((bm[r] + bs[r]).max())
+        else:
+            cmax = float(morton_decode_host(c[:1]).max() + 1)
+        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.leaves), n, None, cmax)
 
 
 class DeviceShading:
