@@ -15,7 +15,7 @@ import threading
 from .errors import (ContractViolation, DeviceError, DuplicateMortonError, ExtensionMissing)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libartemis.so")
+LIB_PATH = os.environ.get("ARTEMIS_LIB_PATH") or os.path.join(HERE, "libartemis.so")
 
 P = C.c_void_p
 I32 = C.c_int32

@@ -47,8 +47,12 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile csrc/*.cu into `out` (default: the in-tree libartemis.so);
+    `defines` are extra -D flags (tuning variants)."""
+    target = out or LIB
+    if not force and not defines and out is None and not stale():
         return LIB
     cc = nvcc()
     with tempfile.TemporaryDirectory() as tmp:
@@ -56,7 +60,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         procs = []
         for src in sources():
             obj = os.path.join(tmp, os.path.basename(src) + ".o")
-            cmd = [cc, *ARCH, *FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+            cmd = [cc, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC,
+                   "-c", src, "-o", obj]
             procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                                 stderr=subprocess.STDOUT, text=True)))
             objs.append(obj)
@@ -68,13 +73,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed on {src}:\n{out}")
         tmp_lib = os.path.join(tmp, "libartemis.so")
         subprocess.run([cc, *ARCH, "-shared", "-o", tmp_lib, *objs, "-lcudart"], check=True)
-        shutil.copy2(tmp_lib, LIB + ".tmp")
-        os.replace(LIB + ".tmp", LIB)
+        shutil.copy2(tmp_lib, target + ".tmp")
+        os.replace(target + ".tmp", target)
         if verbose:
             print("\n".join(logs))
-        with open(os.path.join(HERE, "ptxas.log"), "w") as fh:
-            fh.write("\n".join(logs))
-    return LIB
+        if out is None:
+            with open(os.path.join(HERE, "ptxas.log"), "w") as fh:
+                fh.write("\n".join(logs))
+    return target
 
 
 if __name__ == "__main__":

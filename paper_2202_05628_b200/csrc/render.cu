@@ -30,14 +30,26 @@
 
 namespace artemis {
 
+#ifndef ARTEMIS_SMEM_STACK
+#define ARTEMIS_SMEM_STACK 32
+#endif
+#ifndef ARTEMIS_QCAP
+#define ARTEMIS_QCAP 8
+#endif
+#ifndef ARTEMIS_QTHRESH
+#define ARTEMIS_QTHRESH 64
+#endif
+#ifndef ARTEMIS_MIN_BLOCKS
+#define ARTEMIS_MIN_BLOCKS 1
+#endif
 namespace {
 constexpr int kRenderWarps = 4;
 constexpr int kRenderThreads = 32 * kRenderWarps;
-constexpr int kSmemStack = 32;       // per-thread stack entries kept in shared memory
+constexpr int kSmemStack = ARTEMIS_SMEM_STACK;  // per-thread stack entries in shared memory
 constexpr int kStack = 68;           // tree depth <= 64 key bits + super-root; overflow in local
 constexpr int kStackBytes = kSmemStack * kRenderThreads * 4;
-constexpr int kQCap = 8;             // leaves queued per lane per round
-constexpr int kQThresh = 64;         // warp-wide queued leaves that end a traversal phase
+constexpr int kQCap = ARTEMIS_QCAP;  // leaves queued per lane per round
+constexpr int kQThresh = ARTEMIS_QTHRESH;  // warp-wide queued leaves that end a traversal phase
 constexpr int kMaxSteps = 64;        // traversal steps per phase at most
 // per queued leaf: leaf id / FLUT row (4) + t0 (8) + exp(-sigma*delta) (8) + (a, dir) (16)
 constexpr int kQueueBytes = kQCap * kRenderThreads * (4 + 8 + 8 + 16);
@@ -46,6 +58,19 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 }  // namespace
 
 enum RenderMode { kRender = 0, kTrace = 1, kCount = 2 };
+
+#ifdef ARTEMIS_PHASE_CLOCKS
+// per-phase SM cycles summed over warps: refill, A, B1, B2, C, retire, tail
+__device__ unsigned long long g_phase_clocks[8];
+extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
+    cudaMemcpyFromSymbol(out, g_phase_clocks, sizeof(unsigned long long) * 7);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_phase_clocks, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 struct RenderArgs {
     const PackedNode *nodes;
@@ -242,7 +267,7 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
 // the reference's `lt0 <= rt0` comparison yields (_core.pyx:345). Internal
 // tests use the fp32 filter; emitted leaves get exact fp64 intervals.
 template <int kDeg, int kMode, bool kCamera, bool kVec>
-__global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
+__global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_kernel(RenderArgs p) {
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
@@ -253,7 +278,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
     float4 *q_val = reinterpret_cast<float4 *>(qbase + kQCap * kRenderThreads * 20);  // a, dir
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
-    const int cp = kVec ? C + 4 : (C | 1);
+    const int cp = kVec ? C : (C | 1);
     float *feat = reinterpret_cast<float *>(s_raw + kStackBytes + kQueueBytes) +
                   (size_t)warp * 32 * cp;
     if (kMode != kCount)
@@ -263,6 +288,22 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
     const int64_t n_ids = kCamera ? (int64_t)p.tiles_x * p.tiles_y * 32 : p.n_rays;
     const unsigned lt = lanemask_lt();
     const int wbase = warp * 32;  // this warp's column block in the queue arrays
+#ifdef ARTEMIS_PHASE_CLOCKS
+    unsigned long long ph_acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long ph_t = clock64();
+    int ph_cur = 0;
+#define ARTEMIS_PHASE(k)                          \
+    do {                                          \
+        const long long _t = clock64();           \
+        ph_acc[ph_cur] += (unsigned long long)(_t - ph_t); \
+        ph_t = _t;                                \
+        ph_cur = (k) < 6 ? (k) : 6;               \
+    } while (0)
+#else
+#define ARTEMIS_PHASE(k) \
+    do {                 \
+    } while (0)
+#endif
 
     // per-lane ray state
     int64_t ray = -1;
@@ -385,6 +426,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
     const int grp = lane / lph, q = lane % lph;
 
     while (true) {
+        ARTEMIS_PHASE(0);
         // ---- refill idle lanes from the ray queue
         const unsigned idle = __ballot_sync(0xffffffffu, ray < 0);
         if (queue_open && __popc(idle) >= 8) {
@@ -401,6 +443,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
             if (!queue_open) break;
             continue;
         }
+        ARTEMIS_PHASE(1);
         // ---- phase A: uniform DFS steps until enough leaves are queued
         for (int it = 0; it < kMaxSteps; ++it) {
             const bool can = walking && nq < kQCap;
@@ -408,6 +451,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
             if (can) step();
             if (__reduce_add_sync(0xffffffffu, (unsigned)nq) >= (unsigned)kQThresh) break;
         }
+        ARTEMIS_PHASE(2);
         // ---- phase B1: exact intervals and per-leaf terms, warp-cooperative
         __syncwarp();
         for (int k = 0; k < kQCap; ++k) {
@@ -444,6 +488,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
             }
         }
         __syncwarp();
+        ARTEMIS_PHASE(3);
         // ---- phase B2: sequential per-ray integration over own leaves
         for (int k = 0; k < nq; ++k) {
             const int qi = k * kRenderThreads + tid;
@@ -482,6 +527,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
                 break;
             }
         }
+        ARTEMIS_PHASE(4);
         // ---- phase C: shade the visible queued leaves, slot by slot
         if (kMode != kCount) {
             __syncwarp();
@@ -536,6 +582,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
             }
         }
         nq = 0;
+        ARTEMIS_PHASE(5);
         // ---- retire finished rays: scalars per lane, features row by row
         const bool done = ray >= 0 && !walking;
         if (done) {
@@ -566,12 +613,17 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs p) {
         }
         if (done) ray = -1;
     }
+    ARTEMIS_PHASE(6);
+#ifdef ARTEMIS_PHASE_CLOCKS
+    if (lane == 0)
+        for (int k = 0; k < 7; ++k) atomicAdd(&g_phase_clocks[k], ph_acc[k]);
+#endif
 }
 
 template <int kMode, bool kCamera, bool kVec>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
-    const int cp = kVec ? a.channels + 4 : (a.channels | 1);
+    const int cp = kVec ? a.channels : (a.channels | 1);
     const size_t smem = kStackBytes + kQueueBytes +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4);
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);

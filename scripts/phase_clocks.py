@@ -1,0 +1,27 @@
+"""Render c2 frames with the phase-clock variant and print the phase split."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2202_05628_b200 import _lib  # noqa: E402
+from paper_2202_05628_b200 import kinematics as KM  # noqa: E402
+from paper_2202_05628_b200 import synthetic as S  # noqa: E402
+from paper_2202_05628_b200.frame import FramePipeline  # noqa: E402
+
+sc = S.make_scene("c3", frames=3)
+fp = FramePipeline.from_scene(sc)
+L = _lib.load_library()
+fn = L.artemis_debug_phase_clocks
+fn.argtypes = [C.c_void_p, C.c_int]
+buf = (C.c_ulonglong * 7)()
+for f in range(3):
+    fp.run(KM.PoseSpec.make(sc.poses[f]), sc.cameras[f][0], graph=False)
+    torch.cuda.synchronize()
+    fn(C.addressof(buf), 1)
+vals = list(buf)
+tot = sum(vals)
+names = ["refill", "A traverse", "B1 exact", "B2 chain", "C shade", "retire", "tail"]
+print(" ".join(f"{n}={v / tot * 100:.1f}%" for n, v in zip(names, vals)))
