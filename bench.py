@@ -296,14 +296,14 @@ def main():
     R, origin = cam0.cam_to_world()
     og, dg, dw = K.camera_rays_device(R, origin, cam0.fx, cam0.fy, cam0.cx, cam0.cy, W, H,
                                       sc.lo, sc.cell_size)
+    shade = K.DeviceShading(np.zeros((sc.n_voxels, 2)), np.zeros(sc.n_voxels, np.int32),
+                            np.eye(3)[None], 0, 1)
     dtree = K.DeviceTree(tree["codes"], tree["flut_idx"], tree["root"], tree["left"],
-                         tree["right"], tree["box_min"], tree["box_size"])
+                         tree["right"], tree["box_min"], tree["box_size"], shade)
     counts = K.count_hits_device(dtree, K.DeviceRays.from_tensors(og, dg, dw))
     total_hits = int(counts.sum().item())
     hit_rays = int((counts > 0).sum().item())
     # rows touched: leaves with at least one hit (trace of the frame)
-    shade = K.DeviceShading(np.zeros((sc.n_voxels, 2)), np.zeros(sc.n_voxels, np.int32),
-                            np.eye(3)[None], 0, 1)
     _, _, _, hidx, _, _ = K.forward_fit_device(dtree, shade, K.DeviceRays.from_tensors(og, dg, dw))
     unique_rows = int(torch.unique(hidx).numel())
     del og, dg, dw, dtree, shade, hidx

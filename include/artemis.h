@@ -91,12 +91,15 @@ int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *left, int32_t 
  * The render kernels walk a packed copy of the tree: one 32-byte record per
  * internal node holding both children's boxes (so a visit is one sector),
  * plus a super-root record at index max(n-1, 0) whose left child is the
- * root, and one 16-byte record per leaf {x, y, z, flut row}. Built from the
- * reference arrays (API path) or directly by artemis_frame_run (device
- * pipeline). nodes: n x 32 bytes, leaves: n x 16 bytes. */
+ * root, and one 32-byte record per leaf {x, y, z, flut row, density,
+ * rotation index}. Built from the reference arrays (API path) or directly
+ * by artemis_frame_run (device pipeline). sigma/rot_index are indexed by
+ * FLUT row and may be NULL for trees that are only traversed (not shaded).
+ * nodes: n x 32 bytes, leaves: n x 32 bytes. */
 int artemis_pack_tree(const uint64_t *codes, const uint32_t *flut_idx, int64_t n, int32_t root,
                       const int32_t *left, const int32_t *right, const int32_t *box_min,
-                      const int32_t *box_size, void *nodes, void *leaves, artemis_stream stream);
+                      const int32_t *box_size, const double *sigma, const int32_t *rot_index,
+                      void *nodes, void *leaves, artemis_stream stream);
 
 /* FLUT (n, width) row-major -> fp32 coefficients (n, width-1) + fp64
  * density (n). Replaces the FLUT.data gather layout of _core.pyx:536-551. */

@@ -71,7 +71,7 @@ _SIGS = {
     "artemis_sort_pairs_u64": (INT, [P, P, P, P, I64, INT, P, SZ, P]),
     "artemis_sort_pairs_u32": (INT, [P, P, P, P, I64, INT, P, SZ, P]),
     "artemis_build_tree": (INT, [P, I64, P, P, P, P, P, P]),
-    "artemis_pack_tree": (INT, [P, P, I64, I32, P, P, P, P, P, P, P]),
+    "artemis_pack_tree": (INT, [P, P, I64, I32, P, P, P, P, P, P, P, P, P]),
     "artemis_flut_split_f64": (INT, [P, I64, INT, P, P, P]),
     "artemis_flut_split_f32": (INT, [P, I64, INT, P, P, P]),
     "artemis_render_rays": (INT, [C.POINTER(TreeView), C.POINTER(Shading), C.POINTER(Rays), DBL,

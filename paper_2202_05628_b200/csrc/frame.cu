@@ -114,7 +114,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         mark(3);
         rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
                                          f->n, write_ref ? f->left : nullptr, f->right, f->bmin,
-                                         f->bsize, f->nodes, f->leaves, f->winners, nullptr, st);
+                                         f->bsize, f->nodes, f->leaves, f->winners, as.sigma,
+                                         f->rot_joint, nullptr, st);
     } else {
         rc = sort_pairs<u64>((const u64 *)f->keys, f->vals, (u64 *)f->keys_sorted, f->vals_sorted,
                              f->n, f->key_bits, f->sort_ws, f->sort_ws_bytes, st);
@@ -127,7 +128,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         mark(3);
         rc = launch_build_tree<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n,
                                     write_ref ? f->left : nullptr, f->right, f->bmin, f->bsize,
-                                    f->nodes, f->leaves, f->winners, nullptr, st);
+                                    f->nodes, f->leaves, f->winners, as.sigma, f->rot_joint,
+                                    nullptr, st);
     }
     if (rc) return rc;
     mark(4);
@@ -181,7 +183,7 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->bmin, n * 12);
     rc = rc ? rc : dev_alloc(&f->bsize, n * 12);
     rc = rc ? rc : dev_alloc(&f->nodes, (n + 1) * sizeof(PackedNode));
-    rc = rc ? rc : dev_alloc(&f->leaves, (n + 1) * sizeof(uint4));
+    rc = rc ? rc : dev_alloc(&f->leaves, 2 * (n + 1) * sizeof(uint4));
     f->sort_ws_bytes = sort_workspace_bytes(n, f->key_bits, f->key_bytes);
     f->resolve_ws_bytes = resolve_workspace_bytes(n);
     rc = rc ? rc : dev_alloc(&f->sort_ws, f->sort_ws_bytes);

@@ -145,6 +145,10 @@ struct RayF {
     bool exact_only;         // some d == 0: every test takes the exact path
 };
 
+__device__ __forceinline__ void prefetch_l2(const void *ptr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
 __device__ __forceinline__ float int_to_float_exact(uint32_t v) {
     // v < 2^23: place v in the mantissa of 2^23 and subtract (exact, 2 ops)
     return __int_as_float(0x4B000000 | v) - 8388608.0f;
@@ -331,6 +335,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     auto enqueue = [&](int leaf) {
         q_id[nq * kRenderThreads + tid] = (uint32_t)leaf;
         ++nq;
+        prefetch_l2(p.leaves + 2 * (size_t)leaf);  // its record is read in phase B1
     };
     // one DFS step (_core.pyx:307-355 order)
     auto step = [&]() {
@@ -468,17 +473,22 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
             if (src < 32) {
                 const int qi = k * kRenderThreads + wbase + (int)src;
-                const uint4 L = __ldg(p.leaves + q_id[qi]);
+                const uint4 L = __ldg(p.leaves + 2 * (size_t)q_id[qi]);
                 if (kMode == kCount) continue;
+                const uint4 L2 = __ldg(p.leaves + 2 * (size_t)q_id[qi] + 1);
+                const uint32_t fidx = L.w;
+                {   // the row's 9 x 128 B lines are read in phase C
+                    const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
+                    for (int off = 0; off < p.coef_stride * 4; off += 128) prefetch_l2(row + off);
+                }
                 double t0 = 0.0, t1 = 0.0;
                 clip_exact(L.x, L.y, L.z, so, sd, p.t_min, p.t_max, t0, t1);
-                const uint32_t fidx = L.w;
-                const double sigma = __ldg(p.sigma + fidx);
+                const double sigma = __longlong_as_double(((long long)L2.y << 32) | L2.x);
                 q_id[qi] = fidx | (sigma > p.sigma_dep ? kDenseFlag : 0u);
                 q_t0[qi] = t0;
                 // trace mode keeps t1 for B2, which writes the CSR trace
                 q_em[qi] = kMode == kTrace ? t1 : exp(-sigma * (t1 - t0));
-                const double *R = p.rot_inv + 9 * __ldg(p.rot_index + fidx);
+                const double *R = p.rot_inv + 9 * L2.z;
                 float4 v;
                 v.x = 0.0f;
                 v.y = (float)(R[0] * sw[0] + R[1] * sw[1] + R[2] * sw[2]);
@@ -505,7 +515,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 p.hit_idx[trace_base + hits] = (int64_t)fidx;
                 p.hit_t0[trace_base + hits] = t0;
                 p.hit_t1[trace_base + hits] = t1;
-                em = exp(-__ldg(p.sigma + fidx) * (t1 - t0));
+                em = exp(-__ldg(p.sigma + fidx) * (t1 - t0));  // trace mode: recompute
             } else {
                 em = q_em[qi];
             }

@@ -40,6 +40,18 @@ __device__ __forceinline__ int prefix_len(const K *__restrict__ c, int64_t n, in
     return x ? __clzll((long long)x) : 64;
 }
 
+// 32-byte leaf record: {x, y, z, FLUT row} + {density (fp64), rotation
+// index, 0}, so the render kernel gets everything a hit needs in one sector.
+__device__ __forceinline__ void write_leaf(uint4 *leaves, int64_t i, u64 c, uint32_t row,
+                                           const double *sigma, const int32_t *rot_index) {
+    const double sg = sigma ? sigma[row] : 0.0;
+    const unsigned long long sb = (unsigned long long)__double_as_longlong(sg);
+    leaves[2 * i] = make_uint4((uint32_t)compact_bits3(c), (uint32_t)compact_bits3(c >> 1),
+                               (uint32_t)compact_bits3(c >> 2), row);
+    leaves[2 * i + 1] = make_uint4((uint32_t)sb, (uint32_t)(sb >> 32),
+                                   rot_index ? (uint32_t)rot_index[row] : 0u, 0u);
+}
+
 // Karras node i (i < n-1). Writes reference arrays (when non-null) and the
 // packed record; node 0 also writes the super-root record at index n-1.
 template <typename K>
@@ -102,14 +114,11 @@ __global__ void build_tree_kernel(const K *__restrict__ codes, int64_t n_host,
                                   const int32_t *__restrict__ n_dev, int32_t *left, int32_t *right,
                                   int32_t *bmin, int32_t *bsize, PackedNode *nodes,
                                   uint4 *leaves, const uint32_t *__restrict__ leaf_flut,
-                                  int32_t *dup_flag) {
+                                  const double *__restrict__ sigma,
+                                  const int32_t *__restrict__ rot_index, int32_t *dup_flag) {
     int64_t n = n_dev ? (int64_t)*n_dev : n_host;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (leaves && i < n) {
-        u64 c = (u64)codes[i];
-        leaves[i] = make_uint4((uint32_t)compact_bits3(c), (uint32_t)compact_bits3(c >> 1),
-                               (uint32_t)compact_bits3(c >> 2), leaf_flut[i]);
-    }
+    if (leaves && i < n) write_leaf(leaves, i, (u64)codes[i], leaf_flut[i], sigma, rot_index);
     if (n == 1 && i == 0 && nodes) {
         // single leaf: root = ~0, only the super-root record exists
         PackedNode s;
@@ -131,13 +140,10 @@ __global__ void pack_tree_kernel(const u64 *__restrict__ codes,
                                  const int32_t *__restrict__ left, const int32_t *__restrict__ right,
                                  const int32_t *__restrict__ bmin,
                                  const int32_t *__restrict__ bsize, PackedNode *nodes,
-                                 uint4 *leaves) {
+                                 uint4 *leaves, const double *__restrict__ sigma,
+                                 const int32_t *__restrict__ rot_index) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) {
-        u64 c = codes[i];
-        leaves[i] = make_uint4((uint32_t)compact_bits3(c), (uint32_t)compact_bits3(c >> 1),
-                               (uint32_t)compact_bits3(c >> 2), flut_idx[i]);
-    }
+    if (i < n) write_leaf(leaves, i, codes[i], flut_idx[i], sigma, rot_index);
     auto child = [&](uint32_t *w, int32_t link) {
         if (link < 0) {
             u64 c = codes[~link];
@@ -174,21 +180,24 @@ template <typename K>
 int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
                       int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
                       PackedNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
-                      int32_t *dup_flag, cudaStream_t st) {
+                      const double *sigma, const int32_t *rot_index, int32_t *dup_flag,
+                      cudaStream_t st) {
     int64_t threads = n_cap > 1 ? n_cap : 1;
     int blocks = (int)ceil_div<int64_t>(threads, 256);
     build_tree_kernel<K><<<blocks, 256, 0, st>>>(codes, n_host, n_dev, left, right, bmin, bsize,
-                                                  nodes, leaves, leaf_flut, dup_flag);
+                                                  nodes, leaves, leaf_flut, sigma, rot_index,
+                                                  dup_flag);
     return ARTEMIS_LAUNCHED();
 }
 
 template int launch_build_tree<u64>(const u64 *, int64_t, const int32_t *, int64_t, int32_t *,
                                     int32_t *, int32_t *, int32_t *, PackedNode *, uint4 *,
-                                    const uint32_t *, int32_t *, cudaStream_t);
+                                    const uint32_t *, const double *, const int32_t *, int32_t *,
+                                    cudaStream_t);
 template int launch_build_tree<uint32_t>(const uint32_t *, int64_t, const int32_t *, int64_t,
                                          int32_t *, int32_t *, int32_t *, int32_t *,
-                                         PackedNode *, uint4 *, const uint32_t *, int32_t *,
-                                         cudaStream_t);
+                                         PackedNode *, uint4 *, const uint32_t *, const double *,
+                                         const int32_t *, int32_t *, cudaStream_t);
 
 }  // namespace artemis
 
@@ -220,18 +229,20 @@ extern "C" int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *lef
     if (n == 1) return ARTEMIS_OK;
     if (!left || !right || !box_min || !box_size) return ARTEMIS_ERR_ARG;
     return launch_build_tree<u64>(reinterpret_cast<const u64 *>(codes), n, nullptr, n, left,
-                                  right, box_min, box_size, nullptr, nullptr, nullptr, dup_flag,
-                                  S(stream));
+                                  right, box_min, box_size, nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, dup_flag, S(stream));
 }
 
 extern "C" int artemis_pack_tree(const uint64_t *codes, const uint32_t *flut_idx, int64_t n,
                                  int32_t root, const int32_t *left, const int32_t *right,
-                                 const int32_t *box_min, const int32_t *box_size, void *nodes,
+                                 const int32_t *box_min, const int32_t *box_size,
+                                 const double *sigma, const int32_t *rot_index, void *nodes,
                                  void *leaves, artemis_stream stream) {
     if (n < 1 || !codes || !flut_idx || !nodes || !leaves) return ARTEMIS_ERR_ARG;
     if (n > 1 && (!left || !right || !box_min || !box_size)) return ARTEMIS_ERR_ARG;
     pack_tree_kernel<<<(int)ceil_div<int64_t>(n, 256), 256, 0, S(stream)>>>(
         reinterpret_cast<const u64 *>(codes), flut_idx, n, root, left, right, box_min, box_size,
-        reinterpret_cast<PackedNode *>(nodes), reinterpret_cast<uint4 *>(leaves));
+        reinterpret_cast<PackedNode *>(nodes), reinterpret_cast<uint4 *>(leaves), sigma,
+        rot_index);
     return ARTEMIS_LAUNCHED();
 }

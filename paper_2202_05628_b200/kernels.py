@@ -122,9 +122,10 @@ def morton_decode_host(codes) -> np.ndarray:
 
 
 class DeviceTree:
-    """A reference-layout tree on the device plus its packed traversal copy."""
+    """A reference-layout tree on the device plus its packed traversal copy
+    (leaf records carry density and rotation index when `shade` is given)."""
 
-    def __init__(self, codes, flut_idx, root, left, right, box_min, box_size):
+    def __init__(self, codes, flut_idx, root, left, right, box_min, box_size, shade=None):
         c = np.ascontiguousarray(codes, dtype=np.uint64).reshape(-1)
         n = c.size
         if n < 1:
@@ -141,10 +142,13 @@ class DeviceTree:
         else:
             self.left = self.right = self.bmin = self.bsize = None
         self.nodes = workspace(32 * n)
-        self.leaves = workspace(16 * n)
+        self.leaves = workspace(32 * n)
+        sig = shade.sigma if shade is not None else None
+        rix = shade.rot_index if shade is not None else None
         check(L.artemis_pack_tree(ptr(self.codes), ptr(self.flut_idx), n, int(root),
                                   ptr(self.left), ptr(self.right), ptr(self.bmin), ptr(self.bsize),
-                                  ptr(self.nodes), ptr(self.leaves), stream_handle()), "pack_tree")
+                                  ptr(sig), ptr(rix), ptr(self.nodes), ptr(self.leaves),
+                                  stream_handle()), "pack_tree")
         if n > 1:
             bm = np.asarray(box_min).reshape(-1, 3)
             bs = np.asarray(box_size).reshape(-1, 3)
@@ -217,8 +221,8 @@ def render_device(tree: DeviceTree, shade: DeviceShading, rays: DeviceRays, lamb
 def render_rays(codes, flut_idx, root, left, right, box_min, box_size, origins_g, dirs_g,
                 dirs_w, t_min, t_max, flut, rot_index, rot_inv, degree, channels, lambda_th,
                 sigma_dep, early_stop, nthreads=1):
-    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size)
     shade = DeviceShading(flut, rot_index, rot_inv, degree, channels)
+    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size, shade)
     rays = DeviceRays(origins_g, dirs_g, dirs_w, t_min, t_max)
     F, A, D = render_device(tree, shade, rays, lambda_th, sigma_dep, early_stop)
     return download(F).astype(np.float64), download(A), download(D)
@@ -255,8 +259,8 @@ def forward_fit_device(tree: DeviceTree, shade: DeviceShading, rays: DeviceRays)
 
 def forward_fit(codes, flut_idx, root, left, right, box_min, box_size, origins_g, dirs_g,
                 dirs_w, t_min, t_max, flut, rot_index, rot_inv, degree, channels, nthreads=1):
-    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size)
     shade = DeviceShading(flut, rot_index, rot_inv, degree, channels)
+    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size, shade)
     rays = DeviceRays(origins_g, dirs_g, dirs_w, t_min, t_max)
     F, A, off, hi, h0, h1 = forward_fit_device(tree, shade, rays)
     return (download(F).astype(np.float64), download(A), off, download(hi), download(h0),
@@ -265,11 +269,11 @@ def forward_fit(codes, flut_idx, root, left, right, box_min, box_size, origins_g
 
 def traverse_ray(codes, flut_idx, root, left, right, box_min, box_size, origin_g, dir_g,
                  t_min, t_max):
-    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size)
     fi = np.asarray(flut_idx)
     rows = int(fi.max()) + 1 if fi.size else 1
     # trace-only: zero density and a 1-channel degree-0 table (no shading work)
     shade = DeviceShading(np.zeros((rows, 2)), np.zeros(rows, np.int32), np.eye(3)[None], 0, 1)
+    tree = DeviceTree(codes, flut_idx, root, left, right, box_min, box_size, shade)
     rays = DeviceRays(np.asarray(origin_g).reshape(1, 3), np.asarray(dir_g).reshape(1, 3), None,
                       t_min, t_max)
     _, _, _, hi, h0, h1 = forward_fit_device(tree, shade, rays)

@@ -271,9 +271,9 @@ def render_view(octree, flut, warp, camera, options=None):
     og, dg, dw = K.camera_rays_device(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
                                       cam.height, lo, cell)
     rot_index, rot_inv = _rotation_tables(warp, len(flut))
-    tree = K.DeviceTree(octree.codes, octree.flut_idx, octree.root, octree.left, octree.right,
-                        octree.box_min, octree.box_size)
     shade = K.DeviceShading(flut.data, rot_index, rot_inv, flut.degree, flut.channels)
+    tree = K.DeviceTree(octree.codes, octree.flut_idx, octree.root, octree.left, octree.right,
+                        octree.box_min, octree.box_size, shade)
     rays = K.DeviceRays.from_tensors(og, dg, dw, 0.0, np.inf)
     F, A, D = K.render_device(tree, shade, rays, opts.lambda_th, opts.sigma_dep, True)
     h, w = cam.height, cam.width

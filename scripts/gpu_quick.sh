@@ -4,3 +4,4 @@ make -s -C oracle
 timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench.log 2>&1; echo bench=$?
 tail -5 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ms/frame', d['ms_per_step'], 'stages', d['stage_ms'], 'frac', d['roofline']['frac'])"
+ARTEMIS_LIB_PATH=$PWD/variants/libartemis_clocks.so timeout 120 python scripts/phase_clocks.py 2>&1 | tail -1
