@@ -144,6 +144,11 @@ typedef struct {
     double fx, fy, cx, cy;
     int32_t width, height;
     double lo[3], cell[3];      /* grid bounds min and cell size */
+    int32_t tile_start, tile_stride; /* frame pipeline: render only the 8x4 pixel
+                                   tiles t with t % tile_stride == tile_start
+                                   (multi-GPU tile sharding); other pixels get
+                                   F = 0, alpha = 0, depth = +inf. 0/0 or 0/1 =
+                                   every tile. */
 } artemis_camera;
 
 /* replaces animvox/_core.pyx:473-559 render_rays. F: (R, C) fp32,

@@ -45,7 +45,7 @@ class Rays(C.Structure):
 class Camera(C.Structure):
     _fields_ = [("R", DBL * 9), ("origin", DBL * 3), ("fx", DBL), ("fy", DBL), ("cx", DBL),
                 ("cy", DBL), ("width", I32), ("height", I32), ("lo", DBL * 3),
-                ("cell", DBL * 3)]
+                ("cell", DBL * 3), ("tile_start", I32), ("tile_stride", I32)]
 
 
 class Asset(C.Structure):

@@ -25,9 +25,9 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
                   int32_t *rot_joint, int32_t *n_in, uint64_t sentinel, int identity,
                   cudaStream_t st);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
-                  const artemis_camera *cam_dev, int width, int height, double lambda_th,
-                  double sigma_dep, int early_stop, float *F, float *A, float *D,
-                  unsigned long long *queue, cudaStream_t st);
+                  const artemis_camera *cam_dev, int width, int height, int sharded,
+                  double lambda_th, double sigma_dep, int early_stop, float *F, float *A,
+                  float *D, unsigned long long *queue, cudaStream_t st);
 
 constexpr int kMaxFrameJoints = 256;
 
@@ -62,6 +62,7 @@ struct artemis_frame_s {
     const void *g_F = nullptr, *g_A = nullptr, *g_D = nullptr;
     cudaStream_t g_stream = nullptr;
     double g_lambda = 0, g_sigma_dep = 0;
+    int g_sharded = 0;
     int launches = 0;
     // stage profiling (eager runs only): events before warp, sort, resolve,
     // build, render and after render
@@ -82,8 +83,8 @@ int dev_alloc(T **p, size_t bytes) {
 }
 
 int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int height,
-                  double lambda_th, double sigma_dep, int flags, float *F, float *A, float *D,
-                  cudaStream_t st) {
+                  int sharded, double lambda_th, double sigma_dep, int flags, float *F, float *A,
+                  float *D, cudaStream_t st) {
     const artemis_asset &as = f->asset;
     int rc;
     int launches = 0;
@@ -138,7 +139,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
-    rc = render_camera(&tv, &sh, &f->params->cam, width, height, lambda_th, sigma_dep,
+    rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
                        flags & 1, F, A, D,
                        reinterpret_cast<unsigned long long *>(f->counters + 2), st);
     mark(5);
@@ -234,22 +235,24 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
         ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, rot_inv, sizeof(double) * 9 * n_joints,
                                     cudaMemcpyHostToDevice, st));
     }
+    const int sharded = cam->tile_stride > 1;
     const int use_graph = (flags & 2) && st != nullptr;
     if (!use_graph)
-        return enqueue_frame(f, identity, n_joints, cam->width, cam->height, lambda_th, sigma_dep,
-                             flags, F, alpha, depth, st);
+        return enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded, lambda_th,
+                             sigma_dep, flags, F, alpha, depth, st);
     const bool same = f->exec && f->g_w == cam->width && f->g_h == cam->height &&
                       f->g_flags == flags && f->g_identity == identity && f->g_nj == n_joints &&
                       f->g_F == F && f->g_A == alpha && f->g_D == depth && f->g_stream == st &&
-                      f->g_lambda == lambda_th && f->g_sigma_dep == sigma_dep;
+                      f->g_lambda == lambda_th && f->g_sigma_dep == sigma_dep &&
+                      f->g_sharded == sharded;
     if (!same) {
         if (f->exec) {
             cudaGraphExecDestroy(f->exec);
             f->exec = nullptr;
         }
         ARTEMIS_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        int rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, lambda_th,
-                               sigma_dep, flags, F, alpha, depth, st);
+        int rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded,
+                               lambda_th, sigma_dep, flags, F, alpha, depth, st);
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(st, &g);
         if (rc) {
@@ -278,6 +281,7 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
         f->g_stream = st;
         f->g_lambda = lambda_th;
         f->g_sigma_dep = sigma_dep;
+        f->g_sharded = sharded;
     }
     ARTEMIS_TRY(cudaGraphLaunch(f->exec, st));
     return ARTEMIS_OK;

@@ -289,7 +289,14 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         for (int i = lane; i < 32 * cp; i += 32) feat[i] = 0.0f;
     const int64_t n_leaves = p.n_leaves_dev ? (int64_t)*p.n_leaves_dev : p.n_leaves;
     const int super_root = (int)(n_leaves > 1 ? n_leaves - 1 : 0);
-    const int64_t n_ids = kCamera ? (int64_t)p.tiles_x * p.tiles_y * 32 : p.n_rays;
+    int tstart = 0, tstride = 1;
+    if (kCamera && p.cam->tile_stride > 1) {
+        tstart = p.cam->tile_start;
+        tstride = p.cam->tile_stride;
+    }
+    const int64_t n_tiles = (int64_t)p.tiles_x * p.tiles_y;
+    const int64_t n_ids = kCamera ? (tstart < n_tiles ? (n_tiles - tstart + tstride - 1) / tstride : 0) * 32
+                                  : p.n_rays;
     const unsigned lt = lanemask_lt();
     const int wbase = warp * 32;  // this warp's column block in the queue arrays
 #ifdef ARTEMIS_PHASE_CLOCKS
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         ray = -1;
         if (kCamera) {
             const artemis_camera &cam = *p.cam;
-            const int64_t tile = id >> 5;
+            const int64_t tile = tstart + (id >> 5) * tstride;
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
             const int py = (int)(tile / p.tiles_x) * 4 + (sl >> 3);
@@ -691,17 +698,29 @@ static void fill_rays(RenderArgs &a, const artemis_rays *r) {
     a.t_max = r->t_max;
 }
 
+__global__ void fill_alpha_depth(float *A, float *D, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        A[i] = 0.0f;
+        D[i] = CUDART_INF_F;
+    }
+}
+
 // Device-pipeline render with in-kernel camera rays (frame.cu).
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
-                  const artemis_camera *cam_dev, int width, int height, double lambda_th,
-                  double sigma_dep, int early_stop, float *F, float *A, float *D,
-                  unsigned long long *queue, cudaStream_t st) {
+                  const artemis_camera *cam_dev, int width, int height, int sharded,
+                  double lambda_th, double sigma_dep, int early_stop, float *F, float *A,
+                  float *D, unsigned long long *queue, cudaStream_t st) {
     RenderArgs a{};
     fill_tree(a, tree);
     fill_shade(a, shade);
     a.cam = cam_dev;
     a.queue = queue;
     ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)width * height * shade->channels * sizeof(float), st));
+    if (sharded) {  // pixels of other ranks' tiles: alpha 0, depth +inf
+        const int64_t n = (int64_t)width * height;
+        fill_alpha_depth<<<(int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148), 256, 0, st>>>(A, D, n);
+    }
     a.tiles_x = (width + 7) / 8;
     a.tiles_y = (height + 3) / 4;
     a.n_rays = (int64_t)width * height;

@@ -117,11 +117,14 @@ class FramePipeline:
 
     def run(self, pose, camera, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
             early_stop: bool = True, graph: bool = True, parity: bool = False, tables=None,
-            out=None):
+            out=None, tiles: tuple | None = None):
         """Enqueue one frame on self.stream; returns device (F, alpha, depth)
-        (fp32, row-major pixels). `pose` None renders the canonical cells."""
+        (fp32, row-major pixels). `pose` None renders the canonical cells.
+        `tiles` = (start, stride) renders only that tile shard (parallel.py)."""
         L = _lib.lib()
         cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
+        if tiles is not None:
+            cam.tile_start, cam.tile_stride = int(tiles[0]), int(tiles[1])
         if pose is None or self.rig is None:
             aff = rot = None
             nj = 1

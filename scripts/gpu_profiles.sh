@@ -1,0 +1,11 @@
+# Round profiles: per-launch device times of one eager frame (all kernels) and
+# a full ncu capture of the render kernel. Run on ONE GPU.
+set -x
+cd "$GRAFT_REPO_ROOT"
+timeout 300 python scripts/prof_frame.py c2 3 > gpurun_out/prof_plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -s 20 --csv --log-file gpurun_out/launches.csv python scripts/prof_frame.py c2 3 > gpurun_out/ncu_launches.log 2>&1
+echo launches=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_render python scripts/prof_frame.py c2 3 > gpurun_out/ncu_render.log 2>&1
+echo ncu=$?
