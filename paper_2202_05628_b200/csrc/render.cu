@@ -25,22 +25,24 @@
 #include <math.h>
 #include <math_constants.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tree.cuh"
 
 namespace artemis {
 
 #ifndef ARTEMIS_SMEM_STACK
-#define ARTEMIS_SMEM_STACK 32
+#define ARTEMIS_SMEM_STACK 28
 #endif
 #ifndef ARTEMIS_QCAP
-#define ARTEMIS_QCAP 8
+#define ARTEMIS_QCAP 6
 #endif
 #ifndef ARTEMIS_QTHRESH
 #define ARTEMIS_QTHRESH 64
 #endif
 #ifndef ARTEMIS_MIN_BLOCKS
-#define ARTEMIS_MIN_BLOCKS 1
+#define ARTEMIS_MIN_BLOCKS 4
 #endif
 namespace {
 constexpr int kRenderWarps = 4;
@@ -51,8 +53,11 @@ constexpr int kStackBytes = kSmemStack * kRenderThreads * 4;
 constexpr int kQCap = ARTEMIS_QCAP;  // leaves queued per lane per round
 constexpr int kQThresh = ARTEMIS_QTHRESH;  // warp-wide queued leaves that end a traversal phase
 constexpr int kMaxSteps = 64;        // traversal steps per phase at most
-// per queued leaf: leaf id / FLUT row (4) + t0 (8) + exp(-sigma*delta) (8) + (a, dir) (16)
-constexpr int kQueueBytes = kQCap * kRenderThreads * (4 + 8 + 8 + 16);
+// per queued leaf: leaf id / FLUT row (4) + exp(-sigma*delta) (8) + (a, dir) (16) + entry
+// distance t0 (fp32 in the frame pipeline, whose depth buffer is fp32; fp64 otherwise)
+constexpr int queue_bytes(bool fp32_t0) {
+    return kQCap * kRenderThreads * (4 + 8 + 16 + (fp32_t0 ? 4 : 8));
+}
 constexpr uint32_t kDenseFlag = 1u << 31;  // queued row's density exceeds sigma_dep
 constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~leaf)
 }  // namespace
@@ -275,11 +280,13 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
+    using T0 = typename std::conditional<kCamera, float, double>::type;
+    constexpr int kQueueBytes = queue_bytes(kCamera);
     unsigned char *qbase = s_raw + kStackBytes;
     uint32_t *q_id = reinterpret_cast<uint32_t *>(qbase);                            // leaf, then row
-    double *q_t0 = reinterpret_cast<double *>(qbase + kQCap * kRenderThreads * 4);
-    double *q_em = reinterpret_cast<double *>(qbase + kQCap * kRenderThreads * 12);
-    float4 *q_val = reinterpret_cast<float4 *>(qbase + kQCap * kRenderThreads * 20);  // a, dir
+    double *q_em = reinterpret_cast<double *>(qbase + kQCap * kRenderThreads * 4);
+    float4 *q_val = reinterpret_cast<float4 *>(qbase + kQCap * kRenderThreads * 12);  // a, dir
+    T0 *q_t0 = reinterpret_cast<T0 *>(qbase + kQCap * kRenderThreads * 28);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
     const int cp = kVec ? C : (C | 1);
@@ -492,7 +499,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 clip_exact(L.x, L.y, L.z, so, sd, p.t_min, p.t_max, t0, t1);
                 const double sigma = __longlong_as_double(((long long)L2.y << 32) | L2.x);
                 q_id[qi] = fidx | (sigma > p.sigma_dep ? kDenseFlag : 0u);
-                q_t0[qi] = t0;
+                q_t0[qi] = (T0)t0;
                 // trace mode keeps t1 for B2, which writes the CSR trace
                 q_em[qi] = kMode == kTrace ? t1 : exp(-sigma * (t1 - t0));
                 const double *R = p.rot_inv + 9 * L2.z;
@@ -515,7 +522,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 continue;
             }
             const uint32_t fidx = id & ~kDenseFlag;
-            const double t0 = q_t0[qi];
+            const double t0 = (double)q_t0[qi];
             double em;
             if (kMode == kTrace) {
                 const double t1 = q_em[qi];
@@ -641,7 +648,7 @@ template <int kMode, bool kCamera, bool kVec>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
-    const size_t smem = kStackBytes + kQueueBytes +
+    const size_t smem = kStackBytes + queue_bytes(kCamera) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4);
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {

@@ -1,5 +1,4 @@
 """Build libartemis tuning variants into variants/ (git-ignored)."""
-import itertools
 import os
 import sys
 
@@ -8,13 +7,15 @@ from paper_2202_05628_b200 import build_lib  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "q4": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48"),
-    "q4s24": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48", "ARTEMIS_SMEM_STACK=24"),
-    "q4s24b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48", "ARTEMIS_SMEM_STACK=24",
-                "ARTEMIS_MIN_BLOCKS=5"),
-    "q6t96": ("ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=96"),
-    "q8t128": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=128"),
-    "q8t32": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=32"),
+    "s24q8": ("ARTEMIS_SMEM_STACK=24",),
+    "s24q6": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=64"),
+    "s24q6b4": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=64",
+                "ARTEMIS_MIN_BLOCKS=4"),
+    "s28q6b4": ("ARTEMIS_SMEM_STACK=28", "ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=64",
+                "ARTEMIS_MIN_BLOCKS=4"),
+    "s24q5b4": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=48",
+                "ARTEMIS_MIN_BLOCKS=4"),
+    "s24q8t96": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QTHRESH=96"),
 }
 names = sys.argv[1:] or list(VARIANTS)
 repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
