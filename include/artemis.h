@@ -95,7 +95,7 @@ int artemis_build_tree(const uint64_t *codes, int64_t n, int32_t *left, int32_t 
  * rotation index}. Built from the reference arrays (API path) or directly
  * by artemis_frame_run (device pipeline). sigma/rot_index are indexed by
  * FLUT row and may be NULL for trees that are only traversed (not shaded).
- * nodes: n x 32 bytes, leaves: n x 32 bytes. */
+ * nodes: n x 64 bytes (two-level records), leaves: n x 32 bytes. */
 int artemis_pack_tree(const uint64_t *codes, const uint32_t *flut_idx, int64_t n, int32_t root,
                       const int32_t *left, const int32_t *right, const int32_t *box_min,
                       const int32_t *box_size, const double *sigma, const int32_t *rot_index,

@@ -89,6 +89,15 @@ struct PackedNode {
     uint32_t w[8];
 };
 
+// Traversal record of one internal node (64 bytes): its four grandchild
+// slots in left-to-right order {LL, LR, RL, RR}, each a packed box + link
+// (when a child is a leaf it takes slot 0 or 2 and slot 1 or 3 is absent).
+// Split axes: the node's in slot 0 bits 27-28, the left child's in slot 1,
+// the right child's in slot 3. One visit covers two binary levels.
+struct WideNode {
+    uint4 s[4];
+};
+
 __host__ __device__ __forceinline__ int box_size_axis(int free_bits, int axis) {
     return 1 << ((free_bits + 2 - axis) / 3);
 }

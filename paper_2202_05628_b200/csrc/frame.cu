@@ -51,7 +51,7 @@ struct artemis_frame_s {
     uint32_t *vals = nullptr, *vals_sorted = nullptr, *winners = nullptr;
     int32_t *rot_joint = nullptr, *counters = nullptr;
     int32_t *left = nullptr, *right = nullptr, *bmin = nullptr, *bsize = nullptr;
-    PackedNode *nodes = nullptr;
+    WideNode *nodes = nullptr;
     uint4 *leaves = nullptr;
     void *sort_ws = nullptr, *resolve_ws = nullptr;
     size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
@@ -183,7 +183,7 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->right, n * 4);
     rc = rc ? rc : dev_alloc(&f->bmin, n * 12);
     rc = rc ? rc : dev_alloc(&f->bsize, n * 12);
-    rc = rc ? rc : dev_alloc(&f->nodes, (n + 1) * sizeof(PackedNode));
+    rc = rc ? rc : dev_alloc(&f->nodes, (n + 1) * sizeof(WideNode));
     rc = rc ? rc : dev_alloc(&f->leaves, 2 * (n + 1) * sizeof(uint4));
     f->sort_ws_bytes = sort_workspace_bytes(n, f->key_bits, f->key_bytes);
     f->resolve_ws_bytes = resolve_workspace_bytes(n);

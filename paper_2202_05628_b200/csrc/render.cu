@@ -48,7 +48,7 @@ namespace {
 constexpr int kRenderWarps = 4;
 constexpr int kRenderThreads = 32 * kRenderWarps;
 constexpr int kSmemStack = ARTEMIS_SMEM_STACK;  // per-thread stack entries in shared memory
-constexpr int kStack = 68;           // tree depth <= 64 key bits + super-root; overflow in local
+constexpr int kStack = 100;  // <= 3 entries per two-level visit x 32 visits (64-bit keys) + slack
 constexpr int kStackBytes = kSmemStack * kRenderThreads * 4;
 constexpr int kQCap = ARTEMIS_QCAP;  // leaves queued per lane per round
 constexpr int kQThresh = ARTEMIS_QTHRESH;  // warp-wide queued leaves that end a traversal phase
@@ -64,21 +64,10 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 
 enum RenderMode { kRender = 0, kTrace = 1, kCount = 2 };
 
-#ifdef ARTEMIS_PHASE_CLOCKS
-// per-phase SM cycles summed over warps: refill, A, B1, B2, C, retire, tail
-__device__ unsigned long long g_phase_clocks[8];
-extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
-    cudaMemcpyFromSymbol(out, g_phase_clocks, sizeof(unsigned long long) * 7);
-    if (reset) {
-        unsigned long long z[8] = {0};
-        cudaMemcpyToSymbol(g_phase_clocks, z, sizeof(z));
-    }
-    return 0;
-}
-#endif
+
 
 struct RenderArgs {
-    const PackedNode *nodes;
+    const WideNode *nodes;
     const uint4 *leaves;  // {x, y, z, flut row}
     int64_t n_leaves;
     const int32_t *n_leaves_dev;
@@ -142,6 +131,25 @@ __device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2
     return true;
 }
 
+#ifdef ARTEMIS_PHASE_CLOCKS
+// per-phase SM cycles summed over warps: refill, A, B1, B2, C, retire, tail
+__device__ unsigned long long g_phase_clocks[8];
+__device__ unsigned long long g_fallbacks;
+__device__ unsigned long long g_tests;
+extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
+    cudaMemcpyFromSymbol(out, g_phase_clocks, sizeof(unsigned long long) * 7);
+    cudaMemcpyFromSymbol(out + 7, g_fallbacks, sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out + 8, g_tests, sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_phase_clocks, z, sizeof(z));
+        cudaMemcpyToSymbol(g_fallbacks, z, sizeof(unsigned long long));
+        cudaMemcpyToSymbol(g_tests, z, sizeof(unsigned long long));
+    }
+    return 0;
+}
+#endif
+
 // Per-ray constants of the fp32 filtered box test.
 struct RayF {
     float o_inv[3], inv[3];  // o * (1/d) and 1/d in fp32 (axes with d != 0)
@@ -168,6 +176,9 @@ __device__ __forceinline__ float int_to_float_exact(uint32_t v) {
 __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t w2,
                                              const RayF &rf, const double o[3],
                                              const double d[3], double t_min, double t_max) {
+#ifdef ARTEMIS_PHASE_CLOCKS
+    atomicAdd(&g_tests, 1ull);
+#endif
     if (!rf.exact_only) {
         const uint32_t w[3] = {w0, w1, w2};
         float e = -INFINITY, x = INFINITY, ec = 0.0f, xc = 0.0f;
@@ -192,6 +203,9 @@ __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t 
         if (e + m < x && e + m < rf.tmax_dn && rf.tmin_up + m < x) return true;
         if (e > x + m || e > rf.tmax_up + m || rf.tmin_dn > x + m) return false;
     }
+#ifdef ARTEMIS_PHASE_CLOCKS
+    atomicAdd(&g_fallbacks, 1ull);
+#endif
     double e0, e1;
     return clip_exact(w0, w1, w2, o, d, t_min, t_max, e0, e1);
 }
@@ -351,41 +365,64 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         ++nq;
         prefetch_l2(p.leaves + 2 * (size_t)leaf);  // its record is read in phase B1
     };
-    // one DFS step (_core.pyx:307-355 order)
+    // one DFS step (_core.pyx:307-355 order) over a two-level record: test
+    // the (up to) four grandchild slots, order the hit ones as the binary
+    // DFS would (split-axis rule at the node, then inside each child), queue
+    // the leading leaves, push the rest in reverse so they pop in order.
     auto step = [&]() {
         if (cur == kEnd) {
             walking = false;
             return;
         }
-        if (cur < 0) {  // a far leaf, hit-tested before it was pushed
+        if (cur < 0) {  // a leaf, hit-tested before it was pushed
             enqueue(~cur);
             cur = pop();
             return;
         }
-        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur));
-        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p.nodes + cur) + 1);
-        const bool hl = hit_filtered(a.x, a.y, a.z, rf, og, dg, p.t_min, p.t_max);
-        const bool hr =
-            !(b.x & kAbsent) && hit_filtered(b.x, b.y, b.z, rf, og, dg, p.t_min, p.t_max);
-        int nxt;
-        if (hl && hr) {
-            const bool left_first = dg[(a.x >> 27) & 3u] > 0.0;
-            push(left_first ? (int)b.w : (int)a.w);
-            nxt = left_first ? (int)a.w : (int)b.w;
-        } else if (hl) {
-            nxt = (int)a.w;
-        } else if (hr) {
-            nxt = (int)b.w;
-        } else {
-            cur = pop();
-            return;
+        const uint4 *rec = reinterpret_cast<const uint4 *>(p.nodes + cur);
+        const uint4 s0 = __ldg(rec), s1 = __ldg(rec + 1), s2 = __ldg(rec + 2), s3 = __ldg(rec + 3);
+        const bool h0 = hit_filtered(s0.x, s0.y, s0.z, rf, og, dg, p.t_min, p.t_max);
+        const bool h1 = !(s1.x & kAbsent) && hit_filtered(s1.x, s1.y, s1.z, rf, og, dg, p.t_min, p.t_max);
+        const bool h2 = !(s2.x & kAbsent) && hit_filtered(s2.x, s2.y, s2.z, rf, og, dg, p.t_min, p.t_max);
+        const bool h3 = !(s3.x & kAbsent) && hit_filtered(s3.x, s3.y, s3.z, rf, og, dg, p.t_min, p.t_max);
+        const bool left_first = dg[(s0.x >> 27) & 3u] > 0.0;
+        const bool ll_first = dg[(s1.x >> 27) & 3u] > 0.0;  // meaningful when slot 1 exists
+        const bool rl_first = dg[(s3.x >> 27) & 3u] > 0.0;  // meaningful when slot 3 exists
+        // group L = slots (0, 1), group R = slots (2, 3), each in its own order
+        const int la = (int)(ll_first ? s0.w : s1.w), lb = (int)(ll_first ? s1.w : s0.w);
+        const bool hla = ll_first ? h0 : h1, hlb = ll_first ? h1 : h0;
+        const int ra = (int)(rl_first ? s2.w : s3.w), rb = (int)(rl_first ? s3.w : s2.w);
+        const bool hra = rl_first ? h2 : h3, hrb = rl_first ? h3 : h2;
+        int o[4];
+        bool oh[4];
+        o[0] = left_first ? la : ra;
+        oh[0] = left_first ? hla : hra;
+        o[1] = left_first ? lb : rb;
+        oh[1] = left_first ? hlb : hrb;
+        o[2] = left_first ? ra : la;
+        oh[2] = left_first ? hra : hla;
+        o[3] = left_first ? rb : lb;
+        oh[3] = left_first ? hrb : hlb;
+        // compact the hit links in order
+        int e0 = 0, e1 = 0, e2 = 0, e3 = 0, cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (oh[j]) {
+                if (cnt == 0) e0 = o[j];
+                else if (cnt == 1) e1 = o[j];
+                else if (cnt == 2) e2 = o[j];
+                else e3 = o[j];
+                ++cnt;
+            }
         }
-        if (nxt >= 0) {
-            cur = nxt;
-        } else {
-            enqueue(~nxt);
-            cur = pop();
+        auto ent = [&](int j) { return j == 0 ? e0 : j == 1 ? e1 : j == 2 ? e2 : e3; };
+        int j = 0;
+        while (j < cnt && ent(j) < 0 && nq < kQCap) {
+            enqueue(~ent(j));
+            ++j;
         }
+        for (int t = cnt - 1; t >= j; --t) push(ent(t));
+        cur = pop();
     };
     auto start_ray = [&](int64_t id) {
         ray = -1;
@@ -680,7 +717,7 @@ int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream
 }
 
 static void fill_tree(RenderArgs &a, const artemis_tree_view *t) {
-    a.nodes = static_cast<const PackedNode *>(t->nodes);
+    a.nodes = static_cast<const WideNode *>(t->nodes);
     a.leaves = static_cast<const uint4 *>(t->leaves);
     a.n_leaves = t->n_leaves;
     a.n_leaves_dev = t->n_leaves_dev;

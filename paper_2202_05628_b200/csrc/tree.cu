@@ -52,11 +52,51 @@ __device__ __forceinline__ void write_leaf(uint4 *leaves, int64_t i, u64 c, uint
                                    rot_index ? (uint32_t)rot_index[row] : 0u, 0u);
 }
 
+// Split of the Karras node covering the sorted range [first, last]
+// (_core.pyx:233-242): the last index sharing more than the range's common
+// prefix with `first`.
+template <typename K>
+__device__ __forceinline__ int64_t range_split(const K *__restrict__ c, int64_t n, int64_t first,
+                                               int64_t last) {
+    const int node_len = prefix_len(c, n, first, last);
+    int64_t split = first, step = last - first;
+    do {
+        step = (step + 1) >> 1;
+        if (split + step < last && prefix_len(c, n, first, split + step) > node_len)
+            split += step;
+    } while (step > 1);
+    return split;
+}
+
+// The two grandchild slots contributed by child range [a, b].
+template <typename K>
+__device__ __forceinline__ void wide_group(const K *__restrict__ c, int64_t n, int64_t a,
+                                           int64_t b, uint32_t *w) {
+    if (a == b) {  // the child is a leaf: one slot, the other absent
+        pack_child(w, (u64)c[a], (u64)c[a], ~(int32_t)a);
+        w[4] = kAbsent;
+        w[5] = w[6] = w[7] = 0;
+        return;
+    }
+    const int64_t s = range_split(c, n, a, b);
+    pack_child(w, (u64)c[a], (u64)c[s], s == a ? ~(int32_t)s : (int32_t)s);
+    pack_child(w + 4, (u64)c[s + 1], (u64)c[b], s + 1 == b ? ~(int32_t)(s + 1) : (int32_t)(s + 1));
+    w[4] |= (uint32_t)split_axis_of(range_free_bits((u64)c[a], (u64)c[b])) << 27;
+}
+
+__device__ __forceinline__ void store_wide(WideNode *dst, const uint32_t *w) {
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    d[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    d[3] = make_uint4(w[12], w[13], w[14], w[15]);
+}
+
 // Karras node i (i < n-1). Writes reference arrays (when non-null) and the
-// packed record; node 0 also writes the super-root record at index n-1.
+// traversal record; node 0 also writes the super-root record at index n-1.
 template <typename K>
 __device__ void build_node(const K *__restrict__ c, int64_t n, int64_t i, int32_t *left,
-                           int32_t *right, int32_t *bmin, int32_t *bsize, PackedNode *nodes,
+                           int32_t *right, int32_t *bmin, int32_t *bsize, WideNode *nodes,
                            int32_t *dup_flag) {
     int dir = prefix_len(c, n, i, i + 1) > prefix_len(c, n, i, i - 1) ? 1 : -1;
     int floor_len = prefix_len(c, n, i, i - dir);
@@ -90,20 +130,16 @@ __device__ void build_node(const K *__restrict__ c, int64_t n, int64_t i, int32_
         bsize[3 * i + 2] = box_size_axis(fb, 2);
     }
     if (nodes) {
-        PackedNode p;
-        pack_child(p.w, cf, (u64)c[split], l);
-        pack_child(p.w + 4, (u64)c[split + 1], cl, r);
-        p.w[0] |= (uint32_t)split_axis_of(range_free_bits(cf, cl)) << 27;
-        reinterpret_cast<uint4 *>(nodes + i)[0] = make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]);
-        reinterpret_cast<uint4 *>(nodes + i)[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
-        if (i == 0) {
-            PackedNode s;
-            pack_child(s.w, (u64)c[0], (u64)c[n - 1], 0);
-            s.w[4] = kAbsent;
-            s.w[5] = s.w[6] = 0;
-            s.w[7] = 0;
-            reinterpret_cast<uint4 *>(nodes + (n - 1))[0] = make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
-            reinterpret_cast<uint4 *>(nodes + (n - 1))[1] = make_uint4(s.w[4], s.w[5], s.w[6], s.w[7]);
+        uint32_t w[16];
+        wide_group(c, n, first, split, w);
+        wide_group(c, n, split + 1, last, w + 8);
+        w[0] |= (uint32_t)split_axis_of(range_free_bits(cf, cl)) << 27;
+        store_wide(nodes + i, w);
+        if (i == 0) {  // super-root: slot 0 = the root, the rest absent
+            uint32_t sr[16] = {0};
+            pack_child(sr, (u64)c[0], (u64)c[n - 1], 0);
+            sr[4] = sr[8] = sr[12] = kAbsent;
+            store_wide(nodes + (n - 1), sr);
         }
     }
     if (dup_flag && c[i] == c[i + 1]) atomicMin(dup_flag, (int32_t)i);
@@ -112,7 +148,7 @@ __device__ void build_node(const K *__restrict__ c, int64_t n, int64_t i, int32_
 template <typename K>
 __global__ void build_tree_kernel(const K *__restrict__ codes, int64_t n_host,
                                   const int32_t *__restrict__ n_dev, int32_t *left, int32_t *right,
-                                  int32_t *bmin, int32_t *bsize, PackedNode *nodes,
+                                  int32_t *bmin, int32_t *bsize, WideNode *nodes,
                                   uint4 *leaves, const uint32_t *__restrict__ leaf_flut,
                                   const double *__restrict__ sigma,
                                   const int32_t *__restrict__ rot_index, int32_t *dup_flag) {
@@ -121,30 +157,33 @@ __global__ void build_tree_kernel(const K *__restrict__ codes, int64_t n_host,
     if (leaves && i < n) write_leaf(leaves, i, (u64)codes[i], leaf_flut[i], sigma, rot_index);
     if (n == 1 && i == 0 && nodes) {
         // single leaf: root = ~0, only the super-root record exists
-        PackedNode s;
-        u64 c0 = (u64)codes[0];
-        pack_child(s.w, c0, c0, ~0);
-        s.w[4] = kAbsent;
-        s.w[5] = s.w[6] = s.w[7] = 0;
-        reinterpret_cast<uint4 *>(nodes)[0] = make_uint4(s.w[0], s.w[1], s.w[2], s.w[3]);
-        reinterpret_cast<uint4 *>(nodes)[1] = make_uint4(s.w[4], s.w[5], s.w[6], s.w[7]);
+        uint32_t sr[16] = {0};
+        const u64 c0 = (u64)codes[0];
+        pack_child(sr, c0, c0, ~0);
+        sr[4] = sr[8] = sr[12] = kAbsent;
+        store_wide(nodes, sr);
         return;
     }
     if (i >= n - 1) return;
     build_node(codes, n, i, left, right, bmin, bsize, nodes, dup_flag);
 }
 
-// API path: packed records from the reference arrays (any valid tree).
+// API path: traversal records from the reference arrays (any valid tree).
 __global__ void pack_tree_kernel(const u64 *__restrict__ codes,
                                  const uint32_t *__restrict__ flut_idx, int64_t n, int32_t root,
                                  const int32_t *__restrict__ left, const int32_t *__restrict__ right,
                                  const int32_t *__restrict__ bmin,
-                                 const int32_t *__restrict__ bsize, PackedNode *nodes,
+                                 const int32_t *__restrict__ bsize, WideNode *nodes,
                                  uint4 *leaves, const double *__restrict__ sigma,
                                  const int32_t *__restrict__ rot_index) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) write_leaf(leaves, i, codes[i], flut_idx[i], sigma, rot_index);
-    auto child = [&](uint32_t *w, int32_t link) {
+    auto log2i = [](int32_t v) { return (uint32_t)(__ffs(v) - 1); };
+    auto axis_of = [&](int32_t node) {
+        const int32_t *s = bsize + 3 * node;
+        return (uint32_t)split_axis_of((int)(log2i(s[0]) + log2i(s[1]) + log2i(s[2]))) << 27;
+    };
+    auto slot = [&](uint32_t *w, int32_t link) {
         if (link < 0) {
             u64 c = codes[~link];
             w[0] = (uint32_t)compact_bits3(c);
@@ -152,34 +191,41 @@ __global__ void pack_tree_kernel(const u64 *__restrict__ codes,
             w[2] = (uint32_t)compact_bits3(c >> 2);
         } else {
             const int32_t *m = bmin + 3 * link, *s = bsize + 3 * link;
-            w[0] = (uint32_t)m[0] | ((uint32_t)(__ffs(s[0]) - 1) << 21);
-            w[1] = (uint32_t)m[1] | ((uint32_t)(__ffs(s[1]) - 1) << 21);
-            w[2] = (uint32_t)m[2] | ((uint32_t)(__ffs(s[2]) - 1) << 21);
+            w[0] = (uint32_t)m[0] | (log2i(s[0]) << 21);
+            w[1] = (uint32_t)m[1] | (log2i(s[1]) << 21);
+            w[2] = (uint32_t)m[2] | (log2i(s[2]) << 21);
         }
         w[3] = (uint32_t)link;
     };
-    PackedNode p;
+    auto group = [&](uint32_t *w, int32_t child) {
+        if (child < 0) {
+            slot(w, child);
+            w[4] = kAbsent;
+            w[5] = w[6] = w[7] = 0;
+        } else {
+            slot(w, left[child]);
+            slot(w + 4, right[child]);
+            w[4] |= axis_of(child);
+        }
+    };
+    uint32_t w[16] = {0};
     if (i < n - 1) {
-        child(p.w, left[i]);
-        child(p.w + 4, right[i]);
-        const int32_t *s = bsize + 3 * i;
-        const int fb = (__ffs(s[0]) - 1) + (__ffs(s[1]) - 1) + (__ffs(s[2]) - 1);
-        p.w[0] |= (uint32_t)split_axis_of(fb) << 27;
+        group(w, left[i]);
+        group(w + 8, right[i]);
+        w[0] |= axis_of((int32_t)i);
     } else if (i == (n > 1 ? n - 1 : 0)) {
-        child(p.w, root);
-        p.w[4] = kAbsent;
-        p.w[5] = p.w[6] = p.w[7] = 0;
+        slot(w, root);
+        w[4] = w[8] = w[12] = kAbsent;
     } else {
         return;
     }
-    reinterpret_cast<uint4 *>(nodes + i)[0] = make_uint4(p.w[0], p.w[1], p.w[2], p.w[3]);
-    reinterpret_cast<uint4 *>(nodes + i)[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
+    store_wide(nodes + i, w);
 }
 
 template <typename K>
 int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
                       int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
-                      PackedNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
+                      WideNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
                       const double *sigma, const int32_t *rot_index, int32_t *dup_flag,
                       cudaStream_t st) {
     int64_t threads = n_cap > 1 ? n_cap : 1;
@@ -191,12 +237,12 @@ int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int6
 }
 
 template int launch_build_tree<u64>(const u64 *, int64_t, const int32_t *, int64_t, int32_t *,
-                                    int32_t *, int32_t *, int32_t *, PackedNode *, uint4 *,
+                                    int32_t *, int32_t *, int32_t *, WideNode *, uint4 *,
                                     const uint32_t *, const double *, const int32_t *, int32_t *,
                                     cudaStream_t);
 template int launch_build_tree<uint32_t>(const uint32_t *, int64_t, const int32_t *, int64_t,
                                          int32_t *, int32_t *, int32_t *, int32_t *,
-                                         PackedNode *, uint4 *, const uint32_t *, const double *,
+                                         WideNode *, uint4 *, const uint32_t *, const double *,
                                          const int32_t *, int32_t *, cudaStream_t);
 
 }  // namespace artemis
@@ -242,7 +288,7 @@ extern "C" int artemis_pack_tree(const uint64_t *codes, const uint32_t *flut_idx
     if (n > 1 && (!left || !right || !box_min || !box_size)) return ARTEMIS_ERR_ARG;
     pack_tree_kernel<<<(int)ceil_div<int64_t>(n, 256), 256, 0, S(stream)>>>(
         reinterpret_cast<const u64 *>(codes), flut_idx, n, root, left, right, box_min, box_size,
-        reinterpret_cast<PackedNode *>(nodes), reinterpret_cast<uint4 *>(leaves), sigma,
+        reinterpret_cast<WideNode *>(nodes), reinterpret_cast<uint4 *>(leaves), sigma,
         rot_index);
     return ARTEMIS_LAUNCHED();
 }

@@ -7,7 +7,7 @@ namespace artemis {
 template <typename K>
 int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
                       int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
-                      PackedNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
+                      WideNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
                       const double *sigma, const int32_t *rot_index, int32_t *dup_flag,
                       cudaStream_t st);
 

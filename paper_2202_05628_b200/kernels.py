@@ -141,7 +141,7 @@ class DeviceTree:
             self.bsize = upload(np.asarray(box_size).reshape(-1, 3), np.int32)
         else:
             self.left = self.right = self.bmin = self.bsize = None
-        self.nodes = workspace(32 * n)
+        self.nodes = workspace(64 * n)
         self.leaves = workspace(32 * n)
         sig = shade.sigma if shade is not None else None
         rix = shade.rot_index if shade is not None else None
