@@ -306,6 +306,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     const int cp = kVec ? C : (C | 1);
     float *feat = reinterpret_cast<float *>(s_raw + kStackBytes + kQueueBytes) +
                   (size_t)warp * 32 * cp;
+    // per-warp work list (lane | level << 5) used to hand queued leaves to lanes
+    uint16_t *wl = reinterpret_cast<uint16_t *>(
+                       s_raw + kStackBytes + kQueueBytes +
+                       (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4)) +
+                   warp * 32 * kQCap;
     if (kMode != kCount)
         for (int i = lane; i < 32 * cp; i += 32) feat[i] = 0.0f;
     const int64_t n_leaves = p.n_leaves_dev ? (int64_t)*p.n_leaves_dev : p.n_leaves;
@@ -508,24 +513,32 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             if (__reduce_add_sync(0xffffffffu, (unsigned)nq) >= (unsigned)kQThresh) break;
         }
         ARTEMIS_PHASE(2);
-        // ---- phase B1: exact intervals and per-leaf terms, warp-cooperative
+        // ---- phase B1: exact intervals and per-leaf terms, warp-cooperative:
+        // all queued leaves of the warp are listed (lane | level << 5) and
+        // handed out 32 at a time
         __syncwarp();
+        int total = 0;
         for (int k = 0; k < kQCap; ++k) {
             const unsigned m = __ballot_sync(0xffffffffu, nq > k);
             if (!m) break;
-            const unsigned src = __fns(m, 0, lane + 1);  // lane j takes level k's j-th leaf
-            const int sl = src < 32 ? (int)src : lane;
+            if (nq > k) wl[total + __popc(m & lt)] = (uint16_t)(lane | (k << 5));
+            total += __popc(m);
+        }
+        __syncwarp();
+        for (int base = 0; base < total; base += 32) {
+            const bool has = base + lane < total;
+            const int entry = has ? (int)wl[base + lane] : lane;
+            const int src = entry & 31, k = entry >> 5;
             double so[3], sd[3], sw[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                so[a] = __shfl_sync(0xffffffffu, og[a], sl);
-                sd[a] = __shfl_sync(0xffffffffu, dg[a], sl);
-                if (kMode != kCount) sw[a] = __shfl_sync(0xffffffffu, dw[a], sl);
+                so[a] = __shfl_sync(0xffffffffu, og[a], src);
+                sd[a] = __shfl_sync(0xffffffffu, dg[a], src);
+                if (kMode != kCount) sw[a] = __shfl_sync(0xffffffffu, dw[a], src);
             }
-            if (src < 32) {
-                const int qi = k * kRenderThreads + wbase + (int)src;
+            if (has && kMode != kCount) {
+                const int qi = k * kRenderThreads + wbase + src;
                 const uint4 L = __ldg(p.leaves + 2 * (size_t)q_id[qi]);
-                if (kMode == kCount) continue;
                 const uint4 L2 = __ldg(p.leaves + 2 * (size_t)q_id[qi] + 1);
                 const uint32_t fidx = L.w;
                 {   // the row's 9 x 128 B lines are read in phase C
@@ -589,16 +602,20 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
         }
         ARTEMIS_PHASE(4);
-        // ---- phase C: shade the visible queued leaves, slot by slot
+        // ---- phase C: shade the visible queued leaves level by level (a ray
+        // has at most one leaf per level, so its features accumulate in order)
         if (kMode != kCount) {
             __syncwarp();
             for (int k = 0; k < kQCap; ++k) {
-                unsigned m = __ballot_sync(0xffffffffu, nq > k && q_val[k * kRenderThreads + tid].x > 0.0f);
                 if (!__any_sync(0xffffffffu, nq > k)) break;
-                while (m) {
-                    const unsigned src = __fns(m, 0, grp + 1);
-                    if (src < 32) {
-                        const int s = (int)src;
+                const bool vis = nq > k && q_val[k * kRenderThreads + tid].x > 0.0f;
+                const unsigned m = __ballot_sync(0xffffffffu, vis);
+                const int cnt = __popc(m);
+                if (vis) wl[__popc(m & lt)] = (uint16_t)lane;
+                __syncwarp();
+                for (int item = grp; item - grp < cnt; item += hpi) {
+                    if (item < cnt) {
+                        const int s = (int)wl[item];
                         const int qi = k * kRenderThreads + wbase + s;
                         const uint32_t bf = q_id[qi] & ~kDenseFlag;
                         const float4 bv = q_val[qi];
@@ -638,8 +655,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                             }
                         }
                     }
-                    for (int j = 0; j < hpi && m; ++j) m &= m - 1;
                 }
+                __syncwarp();
             }
         }
         nq = 0;
@@ -686,7 +703,8 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
     const size_t smem = kStackBytes + queue_bytes(kCamera) +
-                        (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4);
+                        (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4) +
+                        (size_t)kRenderWarps * 32 * kQCap * 2;
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
