@@ -153,7 +153,7 @@ extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
 // Per-ray constants of the fp32 filtered box test.
 struct RayF {
     float o_inv[3], inv[3];  // o * (1/d) and 1/d in fp32 (axes with d != 0)
-    float c[3];              // |o * (1/d)|: the cancellation scale of each axis
+    float cmax;              // max |o/d| over the axes: the cancellation scale
     float tmin_up, tmin_dn, tmax_up, tmax_dn;
     bool exact_only;         // some d == 0: every test takes the exact path
 };
@@ -167,12 +167,13 @@ __device__ __forceinline__ float int_to_float_exact(uint32_t v) {
     return __int_as_float(0x4B000000 | v) - 8388608.0f;
 }
 
-// Filtered hit test. A plane distance t = (lo - o)/d is evaluated in fp32 as
-// fma(lo, 1/d, -o/d); with 1/d and o/d rounded to fp32 its error is at most
-// 2^-23 (|o/d| + |t|). The entry maximum e and exit minimum x carry the
-// |o/d| of the axis that produced them, and t0 < t1 is decided from (e, x)
-// only when the gap exceeds 4x their combined error bound; otherwise the
-// exact fp64 slab test decides. The answer always equals clip_exact's.
+// Filtered hit test. Each plane distance t = (p - o)/d is evaluated in fp32
+// as fma(p, 1/d, -o/d); with 1/d and o/d rounded to fp32 its error is below
+// 2^-23 (|o/d| + |t|) <= 2^-23 (cmax + |t|), so t0 < t1 is decided from the
+// fp32 entry maximum e and exit minimum x only when their gap exceeds
+// 2^-20 (cmax + |e| + |x|) -- 4x the combined bound -- and otherwise by the
+// exact fp64 slab test. The answer always equals clip_exact's; only its
+// cost differs.
 __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t w2,
                                              const RayF &rf, const double o[3],
                                              const double d[3], double t_min, double t_max) {
@@ -181,7 +182,7 @@ __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t 
 #endif
     if (!rf.exact_only) {
         const uint32_t w[3] = {w0, w1, w2};
-        float e = -INFINITY, x = INFINITY, ec = 0.0f, xc = 0.0f;
+        float e = -INFINITY, x = INFINITY;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const uint32_t lo_i = w[a] & kCoordMask;
@@ -189,17 +190,10 @@ __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t 
             const float hi = int_to_float_exact(lo_i + (1u << ((w[a] >> 21) & 31u)));
             const float ta = fmaf(lo, rf.inv[a], -rf.o_inv[a]);
             const float tb = fmaf(hi, rf.inv[a], -rf.o_inv[a]);
-            const float en = fminf(ta, tb), ex = fmaxf(ta, tb);
-            if (en > e) {
-                e = en;
-                ec = rf.c[a];
-            }
-            if (ex < x) {
-                x = ex;
-                xc = rf.c[a];
-            }
+            e = fmaxf(e, fminf(ta, tb));
+            x = fminf(x, fmaxf(ta, tb));
         }
-        const float m = 4.76837158203125e-07f * (fabsf(e) + fabsf(x) + ec + xc);  // 2^-21
+        const float m = 9.5367431640625e-07f * (rf.cmax + fabsf(e) + fabsf(x));  // 2^-20
         if (e + m < x && e + m < rf.tmax_dn && rf.tmin_up + m < x) return true;
         if (e > x + m || e > rf.tmax_up + m || rf.tmin_dn > x + m) return false;
     }
@@ -452,16 +446,17 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         }
         if (ray < 0) return;
         rf.exact_only = false;
+        rf.cmax = 0.0f;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if (dg[a] == 0.0) {
                 rf.exact_only = true;
-                rf.inv[a] = rf.o_inv[a] = rf.c[a] = 0.0f;
+                rf.inv[a] = rf.o_inv[a] = 0.0f;
             } else {
                 const double inv = 1.0 / dg[a];
                 rf.inv[a] = (float)inv;
                 rf.o_inv[a] = (float)(og[a] * inv);
-                rf.c[a] = fabsf(rf.o_inv[a]);
+                rf.cmax = fmaxf(rf.cmax, fabsf(rf.o_inv[a]));
             }
         }
         rf.tmin_up = __double2float_ru(p.t_min);
