@@ -108,6 +108,25 @@ int artemis_flut_split_f64(const double *flut, int64_t n, int width, float *coef
 int artemis_flut_split_f32(const float *flut, int64_t n, int width, float *coef,
                            double *sigma, artemis_stream stream);
 
+/* Occupancy brick map of a leaf set: dense table of 8^3-cell bricks over
+ * brick coordinates [org, org + dims), 128-byte records (512-bit mask,
+ * per-word prefix counts, first leaf), and the leaf AABB. With it the render
+ * kernels enumerate a ray's hit leaves by an exact cell walk (bricks.cuh
+ * explains why that equals the reference's DFS order). */
+typedef struct {
+    int32_t *table;
+    void *recs;
+    int32_t *aabb;              /* [6] leaf cells: lo xyz inclusive, hi xyz exclusive */
+    int32_t org[3], dims[3];
+} artemis_brickmap;
+
+size_t artemis_brickmap_bytes(int64_t n_leaves, const int32_t *dims /* host [3] */);
+/* codes: sorted unique u64 (n); org/dims host [3] brick-coordinate box that
+ * covers every leaf; storage >= artemis_brickmap_bytes. Fills *out (host). */
+int artemis_brickmap_build(const uint64_t *codes, int64_t n, const int32_t *org,
+                           const int32_t *dims, void *storage, size_t storage_bytes,
+                           artemis_brickmap *out, artemis_stream stream);
+
 typedef struct {
     const void *nodes;          /* artemis_pack_tree output: internal records */
     const void *leaves;         /* artemis_pack_tree output: leaf records */
@@ -116,6 +135,9 @@ typedef struct {
     double coord_max;           /* bound on every box coordinate (the grid
                                    resolution); 0 = 2^21. Only tunes the fp32
                                    filter; results never depend on it. */
+    const artemis_brickmap *bricks; /* host pointer; non-NULL selects the exact
+                                   cell walk instead of the tree DFS (same
+                                   results) */
 } artemis_tree_view;
 
 typedef struct {

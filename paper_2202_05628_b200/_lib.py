@@ -27,9 +27,13 @@ SZ = C.c_size_t
 OK, ERR_ARG, ERR_RANGE, ERR_EMPTY, ERR_DUP, ERR_OOM, ERR_CUDA, ERR_WS, ERR_NODEV = range(9)
 
 
+class BrickMap(C.Structure):
+    _fields_ = [("table", P), ("recs", P), ("aabb", P), ("org", I32 * 3), ("dims", I32 * 3)]
+
+
 class TreeView(C.Structure):
     _fields_ = [("nodes", P), ("leaves", P), ("n_leaves", I64), ("n_leaves_dev", P),
-                ("coord_max", DBL)]
+                ("coord_max", DBL), ("bricks", C.POINTER(BrickMap))]
 
 
 class Shading(C.Structure):
@@ -91,6 +95,8 @@ _SIGS = {
     "artemis_frame_launches": (INT, [P]),
     "artemis_copy_to_host": (INT, [P, P, SZ, P]),
     "artemis_frame_profile": (INT, [P, INT]),
+    "artemis_brickmap_bytes": (SZ, [I64, P]),
+    "artemis_brickmap_build": (INT, [P, I64, P, P, P, SZ, C.POINTER(BrickMap), P]),
     "artemis_frame_stage_ms": (INT, [P, C.POINTER(C.c_float)]),
 }
 

@@ -67,10 +67,10 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
             objs.append(obj)
         logs = []
         for src, p in procs:
-            out, _ = p.communicate()
-            logs.append(out)
+            log, _ = p.communicate()
+            logs.append(log)
             if p.returncode != 0:
-                raise RuntimeError(f"nvcc failed on {src}:\n{out}")
+                raise RuntimeError(f"nvcc failed on {src}:\n{log}")
         tmp_lib = os.path.join(tmp, "libartemis.so")
         subprocess.run([cc, *ARCH, "-shared", "-o", tmp_lib, *objs, "-lcudart"], check=True)
         shutil.copy2(tmp_lib, target + ".tmp")

@@ -1,0 +1,94 @@
+// Occupancy brick map over the sorted unique leaf codes, and the exact cell
+// walk that enumerates a ray's hit leaves with it.
+//
+// Why a cell walk reproduces the reference's tree traversal exactly
+// (_core.pyx:252-355): a leaf is emitted iff its unit cell passes the fp64
+// slab test with t1 > t0 -- every ancestor box contains the cell, so its
+// (monotone, correctly rounded) slab test passes too and the DFS reaches
+// it -- and emitted leaves come out in increasing t0: sibling octants are
+// separated by a plane the ray crosses once, and two distinct cells with
+// positive-length intervals cannot share an entry distance. So the hit
+// sequence is "occupied cells whose exact slab interval is non-empty, in
+// entry order". The walk steps cell to cell across exactly computed plane
+// crossings fl((k - o) / d), the very values the reference's slab test
+// computes, so each visited cell's [max(entries), min(exits)] IS its slab
+// interval; cells are visited in crossing order, tied crossings skip only
+// zero-length cells. Empty 8^3 bricks are skipped in one step: the walk
+// jumps to the brick's exact exit distance and re-derives each axis's slab
+// there with exact crossings.
+#pragma once
+#include "common.cuh"
+
+namespace artemis {
+
+struct BrickRec {
+    uint32_t mask[16];    // 512 occupancy bits, bit = local Morton index (9 bits)
+    uint16_t prefix[16];  // leaves of this brick before word w (valid for words with bits)
+    uint32_t first;       // index of the brick's first leaf in the sorted leaf array
+    uint32_t pad[7];
+};
+
+struct BrickMap {
+    const int32_t *table;  // dense brick table over [org, org + dims) brick coords, -1 = empty
+    const BrickRec *recs;
+    const int32_t *aabb;   // [6] leaf-cell bounds: lo xyz inclusive, hi xyz exclusive
+    int org[3];
+    int dims[3];
+};
+
+__device__ __forceinline__ uint32_t spread3_small(uint32_t v) {  // 3 bits -> slots 0, 3, 6
+    return (v & 1u) | ((v & 2u) << 2) | ((v & 4u) << 4);
+}
+
+__device__ __forceinline__ int brick_lookup(const BrickMap &bm, int bx, int by, int bz) {
+    const int x = bx - bm.org[0], y = by - bm.org[1], z = bz - bm.org[2];
+    if ((unsigned)x >= (unsigned)bm.dims[0] || (unsigned)y >= (unsigned)bm.dims[1] ||
+        (unsigned)z >= (unsigned)bm.dims[2])
+        return -1;
+    return __ldg(bm.table + ((size_t)z * bm.dims[1] + y) * bm.dims[0] + x);
+}
+
+// Exact plane crossing fl((k - o) / d) -- the same double the reference's
+// slab test computes for the plane k of a unit cell.
+__device__ __forceinline__ double crossing(int k, double o, double d) {
+    return __ddiv_rn(__dadd_rn((double)k, -o), d);
+}
+
+// Slab of one axis that contains distance t (entry <= t < exit), searched
+// from an estimate inside [cmin, cmax]; returns its exact entry/exit.
+__device__ __forceinline__ void sync_axis(double o, double d, double t, int cmin, int cmax,
+                                          int &c, double &E, double &X) {
+    const double est = floor(o + t * d);
+    c = est < (double)cmin ? cmin : est > (double)cmax ? cmax : (int)est;
+    if (d > 0.0) {  // slab c = [cross(c), cross(c+1))
+        double lo = crossing(c, o, d);
+        while (c > cmin && lo > t) {
+            --c;
+            lo = crossing(c, o, d);
+        }
+        double hi = crossing(c + 1, o, d);
+        while (c < cmax && hi <= t) {
+            ++c;
+            lo = hi;
+            hi = crossing(c + 1, o, d);
+        }
+        E = lo;
+        X = hi;
+    } else {  // slab c = [cross(c+1), cross(c))
+        double en = crossing(c + 1, o, d);
+        while (c < cmax && en > t) {
+            ++c;
+            en = crossing(c + 1, o, d);
+        }
+        double ex = crossing(c, o, d);
+        while (c > cmin && ex <= t) {
+            --c;
+            en = ex;
+            ex = crossing(c, o, d);
+        }
+        E = en;
+        X = ex;
+    }
+}
+
+}  // namespace artemis

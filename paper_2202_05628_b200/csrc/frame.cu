@@ -14,6 +14,7 @@
 // pose- and camera-independent.
 #include <string.h>
 
+#include "bricks.cuh"
 #include "common.cuh"
 #include "tree.cuh"
 
@@ -53,6 +54,11 @@ struct artemis_frame_s {
     int32_t *left = nullptr, *right = nullptr, *bmin = nullptr, *bsize = nullptr;
     WideNode *nodes = nullptr;
     uint4 *leaves = nullptr;
+    // occupancy brick map (exact cell walk)
+    int32_t *btable = nullptr, *bmeta = nullptr;
+    BrickRec *brecs = nullptr;
+    int bdims[3] = {1, 1, 1};
+    artemis_brickmap bmap{};
     void *sort_ws = nullptr, *resolve_ws = nullptr;
     size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
     FrameParams *params = nullptr;
@@ -133,10 +139,21 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                     nullptr, st);
     }
     if (rc) return rc;
+    {
+        const int org[3] = {0, 0, 0};
+        rc = f->key_bytes == 4
+                 ? build_bricks<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1, f->n,
+                                          org, f->bdims, f->btable, f->brecs, f->bmeta, f->bmeta + 1,
+                                          st)
+                 : build_bricks<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n, org,
+                                     f->bdims, f->btable, f->brecs, f->bmeta, f->bmeta + 1, st);
+        if (rc) return rc;
+        launches += 2;
+    }
     mark(4);
     const int passes = f->key_bits <= 0 ? 1 : (f->key_bits + 7) / 8;
-    launches += 2 + passes + 3 + 1;
-    artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution};
+    launches += 2 + passes + 3 + 1;  // + 2 brick passes counted above
+    artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution, &f->bmap};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
@@ -185,6 +202,19 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->bsize, n * 12);
     rc = rc ? rc : dev_alloc(&f->nodes, (n + 1) * sizeof(WideNode));
     rc = rc ? rc : dev_alloc(&f->leaves, 2 * (n + 1) * sizeof(uint4));
+    for (int k = 0; k < 3; ++k) f->bdims[k] = (a->resolution + 7) / 8;
+    rc = rc ? rc : dev_alloc(&f->btable, (size_t)f->bdims[0] * f->bdims[1] * f->bdims[2] * 4);
+    rc = rc ? rc : dev_alloc(&f->brecs, (size_t)(n + 1) * sizeof(BrickRec));
+    rc = rc ? rc : dev_alloc(&f->bmeta, 64);
+    if (!rc) {
+        f->bmap.table = f->btable;
+        f->bmap.recs = f->brecs;
+        f->bmap.aabb = f->bmeta + 1;
+        for (int k = 0; k < 3; ++k) {
+            f->bmap.org[k] = 0;
+            f->bmap.dims[k] = f->bdims[k];
+        }
+    }
     f->sort_ws_bytes = sort_workspace_bytes(n, f->key_bits, f->key_bytes);
     f->resolve_ws_bytes = resolve_workspace_bytes(n);
     rc = rc ? rc : dev_alloc(&f->sort_ws, f->sort_ws_bytes);
@@ -205,7 +235,7 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
         if (e) cudaEventDestroy(e);
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
-                    f->leaves,
+                    f->leaves, f->btable, f->brecs, f->bmeta,
                     f->sort_ws, f->resolve_ws, f->params};
     for (void *b : bufs)
         if (b) cudaFree(b);

@@ -27,6 +27,7 @@
 
 #include <type_traits>
 
+#include "bricks.cuh"
 #include "common.cuh"
 #include "tree.cuh"
 
@@ -69,6 +70,7 @@ enum RenderMode { kRender = 0, kTrace = 1, kCount = 2 };
 struct RenderArgs {
     const WideNode *nodes;
     const uint4 *leaves;  // {x, y, z, flut row}
+    BrickMap bm;          // exact cell walk (kDDA)
     int64_t n_leaves;
     const int32_t *n_leaves_dev;
     // shading
@@ -283,7 +285,7 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
 // the ray's side of that plane has the smaller entry distance -- the order
 // the reference's `lt0 <= rt0` comparison yields (_core.pyx:345). Internal
 // tests use the fp32 filter; emitted leaves get exact fp64 intervals.
-template <int kDeg, int kMode, bool kCamera, bool kVec>
+template <int kDeg, int kMode, bool kCamera, bool kVec, bool kDDA>
 __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_kernel(RenderArgs p) {
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
@@ -341,6 +343,20 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     bool walking = false;  // DFS not exhausted
     double og[3], dg[3], dw[3];
     RayF rf;
+    // exact cell walk state (kDDA): current cell, step signs, exact entry /
+    // exit crossing per axis, the leaf AABB exit, the cached brick
+    int cc[3] = {0, 0, 0}, cs[3] = {0, 0, 0};
+    double cE[3] = {0, 0, 0}, cX[3] = {0, 0, 0};
+    double t_end = 0.0;
+    int cb[3] = {INT32_MIN, 0, 0}, cbid = -1;
+    int aL[3] = {0, 0, 0}, aU[3] = {0, 0, 0};
+    if (kDDA) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            aL[a] = __ldg(p.bm.aabb + a);
+            aU[a] = __ldg(p.bm.aabb + 3 + a);
+        }
+    }
     double T = 1.0, acc = 0.0, depth = CUDART_INF;
     int64_t hits = 0, trace_base = 0;
     int cur = kEnd, top = 0, nq = 0;
@@ -364,11 +380,113 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         ++nq;
         prefetch_l2(p.leaves + 2 * (size_t)leaf);  // its record is read in phase B1
     };
+    // the cell walk knows the exact interval already: t0, and t1 - t0 (or t1
+    // for the CSR trace)
+    auto enqueue_hit = [&](uint32_t leaf, double t0, double t1) {
+        const int qi = nq * kRenderThreads + tid;
+        q_id[qi] = leaf;
+        q_t0[qi] = (T0)t0;
+        q_em[qi] = kMode == kTrace ? t1 : t1 - t0;
+        ++nq;
+        prefetch_l2(p.leaves + 2 * (size_t)leaf);
+    };
+    // ---- exact cell walk (bricks.cuh)
+    auto walk_advance = [&]() {
+        const double tn = fmin(cX[0], fmin(cX[1], cX[2]));
+        if (!(tn < p.t_max) || !(tn < t_end)) {
+            walking = false;
+            return;
+        }
+        unsigned pend = (cX[0] == tn ? 1u : 0u) | (cX[1] == tn ? 2u : 0u) | (cX[2] == tn ? 4u : 0u);
+        while (pend) {
+            const int k = __ffs(pend) - 1;
+            pend &= pend - 1;
+            const int ck = (k == 0 ? cc[0] : k == 1 ? cc[1] : cc[2]) + (k == 0 ? cs[0] : k == 1 ? cs[1] : cs[2]);
+            const int lk = k == 0 ? aL[0] : k == 1 ? aL[1] : aL[2];
+            const int uk = k == 0 ? aU[0] : k == 1 ? aU[1] : aU[2];
+            if (ck < lk || ck >= uk) {
+                walking = false;
+                return;
+            }
+            const int sk = k == 0 ? cs[0] : k == 1 ? cs[1] : cs[2];
+            const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
+            const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
+            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (a == k) {
+                    cc[a] = ck;
+                    cE[a] = tn;
+                    cX[a] = xn;
+                }
+        }
+    };
+    auto walk_skip_brick = [&]() {
+        double T[3], tb = CUDART_INF;
+        int P[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int b = cc[a] >> 3;
+            P[a] = cs[a] > 0 ? (b + 1) * 8 : b * 8;
+            T[a] = cs[a] != 0 ? crossing(P[a], og[a], dg[a]) : CUDART_INF;
+            tb = fmin(tb, T[a]);
+        }
+        if (!(tb < p.t_max) || !(tb < t_end)) {
+            walking = false;
+            return;
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (cs[a] == 0) continue;
+            if (T[a] == tb) {
+                const int cn = cs[a] > 0 ? P[a] : P[a] - 1;
+                if (cn < aL[a] || cn >= aU[a]) {
+                    walking = false;
+                    return;
+                }
+                cc[a] = cn;
+                cE[a] = tb;
+                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a]);
+            } else {
+                const int b0 = (cc[a] >> 3) * 8;
+                sync_axis(og[a], dg[a], tb, max(b0, aL[a]), min(b0 + 7, aU[a] - 1), cc[a], cE[a],
+                          cX[a]);
+            }
+        }
+    };
+    auto walk_step = [&]() {
+        if (cb[0] != (cc[0] >> 3) || cb[1] != (cc[1] >> 3) || cb[2] != (cc[2] >> 3)) {
+            cb[0] = cc[0] >> 3;
+            cb[1] = cc[1] >> 3;
+            cb[2] = cc[2] >> 3;
+            cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
+        }
+        if (cbid < 0) {
+            walk_skip_brick();
+            return;
+        }
+        const double t0 = fmax(p.t_min, fmax(cE[0], fmax(cE[1], cE[2])));
+        const double t1 = fmin(p.t_max, fmin(cX[0], fmin(cX[1], cX[2])));
+        const uint32_t m = spread3_small(cc[0] & 7) | (spread3_small(cc[1] & 7) << 1) |
+                           (spread3_small(cc[2] & 7) << 2);
+        const BrickRec &R = p.bm.recs[cbid];
+        const uint32_t word = __ldg(&R.mask[m >> 5]);
+        if (((word >> (m & 31u)) & 1u) && t1 > t0) {
+            const uint32_t leaf = __ldg(&R.first) + (uint32_t)__ldg(&R.prefix[m >> 5]) +
+                                  (uint32_t)__popc(word & ((1u << (m & 31u)) - 1u));
+            enqueue_hit(leaf, t0, t1);
+        }
+        walk_advance();
+    };
     // one DFS step (_core.pyx:307-355 order) over a two-level record: test
     // the (up to) four grandchild slots, order the hit ones as the binary
     // DFS would (split-axis rule at the node, then inside each child), queue
     // the leading leaves, push the rest in reverse so they pop in order.
     auto step = [&]() {
+        if constexpr (kDDA) {
+            walk_step();
+            return;
+        }
         if (cur == kEnd) {
             walking = false;
             return;
@@ -472,6 +590,46 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         trace_base = (kMode == kTrace) ? p.offsets[ray] : 0;
         cur = (n_leaves > 0 && p.t_min < p.t_max) ? super_root : kEnd;
         walking = true;
+        if constexpr (kDDA) {
+            // exact slab clip against the leaf AABB, then each axis's slab at
+            // the clipped entry distance
+            walking = false;
+            if (!(n_leaves > 0 && p.t_min < p.t_max)) return;
+            double t0 = p.t_min, t1 = p.t_max;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double lo = (double)aL[a], hi = (double)aU[a];
+                if (dg[a] == 0.0) {
+                    if (og[a] < lo || og[a] >= hi) return;
+                } else {
+                    double ta = __ddiv_rn(__dadd_rn(lo, -og[a]), dg[a]);
+                    double tb = __ddiv_rn(__dadd_rn(hi, -og[a]), dg[a]);
+                    if (ta > tb) {
+                        const double sw = ta;
+                        ta = tb;
+                        tb = sw;
+                    }
+                    if (ta > t0) t0 = ta;
+                    if (tb < t1) t1 = tb;
+                    if (t0 >= t1) return;
+                }
+            }
+            t_end = t1;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (dg[a] == 0.0) {
+                    cs[a] = 0;
+                    cc[a] = (int)floor(og[a]);
+                    cE[a] = -CUDART_INF;
+                    cX[a] = CUDART_INF;
+                } else {
+                    cs[a] = dg[a] > 0.0 ? 1 : -1;
+                    sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
+                }
+            }
+            cb[0] = INT32_MIN;
+            walking = true;
+        }
     };
 
     // cooperative shading geometry: lph lanes per hit, hpi hits per pass
@@ -540,13 +698,18 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                     const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
                     for (int off = 0; off < p.coef_stride * 4; off += 128) prefetch_l2(row + off);
                 }
-                double t0 = 0.0, t1 = 0.0;
-                clip_exact(L.x, L.y, L.z, so, sd, p.t_min, p.t_max, t0, t1);
                 const double sigma = __longlong_as_double(((long long)L2.y << 32) | L2.x);
                 q_id[qi] = fidx | (sigma > p.sigma_dep ? kDenseFlag : 0u);
-                q_t0[qi] = (T0)t0;
-                // trace mode keeps t1 for B2, which writes the CSR trace
-                q_em[qi] = kMode == kTrace ? t1 : exp(-sigma * (t1 - t0));
+                if constexpr (kDDA) {
+                    // interval from the walk; q_em holds t1 - t0 (or t1 for the trace)
+                    if (kMode != kTrace) q_em[qi] = exp(-sigma * q_em[qi]);
+                } else {
+                    double t0 = 0.0, t1 = 0.0;
+                    clip_exact(L.x, L.y, L.z, so, sd, p.t_min, p.t_max, t0, t1);
+                    q_t0[qi] = (T0)t0;
+                    // trace mode keeps t1 for B2, which writes the CSR trace
+                    q_em[qi] = kMode == kTrace ? t1 : exp(-sigma * (t1 - t0));
+                }
                 const double *R = p.rot_inv + 9 * L2.z;
                 float4 v;
                 v.x = 0.0f;
@@ -693,7 +856,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #endif
 }
 
-template <int kMode, bool kCamera, bool kVec>
+template <int kMode, bool kCamera, bool kVec, bool kDDA>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
@@ -704,7 +867,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
     case D: {                                                                                   \
-        auto kern = render_kernel<D, kMode, kCamera, kVec>;                                     \
+        auto kern = render_kernel<D, kMode, kCamera, kVec, kDDA>;                               \
         if (smem > 48 * 1024)                                                                   \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         int occ = 0;                                                                            \
@@ -725,8 +888,16 @@ template <int kMode, bool kCamera>
 int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     const bool vec = kMode != kCount && a.channels % 4 == 0 && a.coef_stride % 4 == 0 &&
                      (reinterpret_cast<uintptr_t>(a.coef) & 15) == 0;
-    return vec ? launch_render_vec<kMode, kCamera, true>(degree, a, warps, st)
-               : launch_render_vec<kMode, kCamera, false>(degree, a, warps, st);
+    const bool dda = a.bm.table != nullptr;
+    if (kCamera) {  // the device pipeline always has a brick map
+        return vec ? launch_render_vec<kMode, kCamera, true, true>(degree, a, warps, st)
+                   : launch_render_vec<kMode, kCamera, false, true>(degree, a, warps, st);
+    }
+    if (dda)
+        return vec ? launch_render_vec<kMode, kCamera, true, true>(degree, a, warps, st)
+                   : launch_render_vec<kMode, kCamera, false, true>(degree, a, warps, st);
+    return vec ? launch_render_vec<kMode, kCamera, true, false>(degree, a, warps, st)
+               : launch_render_vec<kMode, kCamera, false, false>(degree, a, warps, st);
 }
 
 static void fill_tree(RenderArgs &a, const artemis_tree_view *t) {
@@ -735,6 +906,15 @@ static void fill_tree(RenderArgs &a, const artemis_tree_view *t) {
     a.n_leaves = t->n_leaves;
     a.n_leaves_dev = t->n_leaves_dev;
     a.coord_max = t->coord_max > 0.0 ? (float)t->coord_max : 2097152.0f;
+    if (t->bricks) {
+        a.bm.table = t->bricks->table;
+        a.bm.recs = static_cast<const BrickRec *>(t->bricks->recs);
+        a.bm.aabb = t->bricks->aabb;
+        for (int k = 0; k < 3; ++k) {
+            a.bm.org[k] = t->bricks->org[k];
+            a.bm.dims[k] = t->bricks->dims[k];
+        }
+    }
 }
 
 static void fill_shade(RenderArgs &a, const artemis_shading *s) {

@@ -24,4 +24,10 @@ int resolve(const K *sorted_codes, const uint32_t *sorted_idx, int64_t n_host,
             const int32_t *n_dev, const double *sigma, K *live_codes, uint32_t *winners,
             int64_t *pairs, int32_t *n_live, void *ws, size_t ws_bytes, cudaStream_t st);
 
+struct BrickRec;
+template <typename K>
+int build_bricks(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
+                 const int org[3], const int dims[3], int32_t *table, BrickRec *recs,
+                 int32_t *counter, int32_t *aabb, cudaStream_t st);
+
 }  // namespace artemis

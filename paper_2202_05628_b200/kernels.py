@@ -111,6 +111,18 @@ def build_tree(codes, nthreads=1):
     return 0, download(left), download(right), download(bmin), download(bsize)
 
 
+def morton_decode_host_all(codes) -> np.ndarray:
+    """Vectorised host decode (x lowest slot, 21 bits per axis)."""
+    c = np.asarray(codes, dtype=np.uint64)
+    out = np.zeros((c.size, 3), dtype=np.int64)
+    for a in range(3):
+        v = np.zeros(c.size, dtype=np.uint64)
+        for b in range(21):
+            v |= ((c >> np.uint64(3 * b + a)) & np.uint64(1)) << np.uint64(b)
+        out[:, a] = v.astype(np.int64)
+    return out
+
+
 def morton_decode_host(codes) -> np.ndarray:
     """Host decode of a few codes (no device needed)."""
     out = np.zeros((len(codes), 3), dtype=np.int64)
@@ -156,7 +168,30 @@ class DeviceTree:
             cmax = float((bm[r] + bs[r]).max())
         else:
             cmax = float(morton_decode_host(c[:1]).max() + 1)
-        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.leaves), n, None, cmax)
+        self.bmap = None
+        self._bricks(L, c)
+        self.view = _lib.TreeView(ptr(self.nodes), ptr(self.leaves), n, None, cmax,
+                                  C.pointer(self.bmap) if self.bmap is not None else None)
+
+    MAX_BRICK_TABLE = 1 << 24  # entries (64 MB): beyond that the tree DFS is used
+
+    def _bricks(self, L, codes):
+        """Occupancy brick map over the leaves' brick-coordinate box, when it
+        is small enough for a dense table (same results either way)."""
+        xyz = morton_decode_host_all(codes)
+        lo = xyz.min(axis=0) >> 3
+        hi = xyz.max(axis=0) >> 3
+        dims = (hi - lo + 1).astype(np.int32)
+        if int(np.prod(dims.astype(np.int64))) > self.MAX_BRICK_TABLE:
+            return
+        org = np.ascontiguousarray(lo.astype(np.int32))
+        dims = np.ascontiguousarray(dims)
+        self.bstore = workspace(L.artemis_brickmap_bytes(self.n, dims.ctypes.data))
+        bm = _lib.BrickMap()
+        check(L.artemis_brickmap_build(ptr(self.codes), self.n, org.ctypes.data, dims.ctypes.data,
+                                       ptr(self.bstore), self.bstore.numel(), C.byref(bm),
+                                       stream_handle()), "brickmap")
+        self.bmap = bm
 
 
 class DeviceShading:
