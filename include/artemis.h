@@ -257,8 +257,8 @@ int artemis_frame_destroy(artemis_frame frame);
  * pose and camera of the same image size. joint_aff == NULL renders the
  * canonical cells (identity warp, render.py:162-167).
  * flags: bit0 early stop, bit1 capture/replay a CUDA graph (needs a
- * non-default stream), bit2 also write the reference tree arrays
- * (left/right/box_min/box_size) for parity checks.
+ * non-default stream); bit2 is accepted for compatibility (the reference
+ * tree arrays left/right/box_min/box_size are rebuilt every frame).
  * F (W*H, C) fp32, alpha/depth (W*H) fp32, row-major pixels. */
 int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double *rot_inv,
                       int n_joints, const artemis_camera *cam, double lambda_th,
@@ -276,7 +276,7 @@ typedef struct {
     const void *codes;          /* (n_live) Morton codes, code_bytes each */
     int32_t code_bytes;
     const uint32_t *flut_idx;   /* (n_live) */
-    const int32_t *left, *right, *box_min, *box_size; /* (n_live-1[,3]), flags bit2 */
+    const int32_t *left, *right, *box_min, *box_size; /* (n_live-1[,3]) */
     const int32_t *rotation_joint; /* (N) */
     const int32_t *n_live_dev;
     const int32_t *n_in_dev;

@@ -107,7 +107,11 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     if (rc) return rc;
     launches += 1;
     mark(1);
-    const bool write_ref = (flags & 4) != 0;
+    // the Karras tree arrays (reference layout) are rebuilt every frame: they
+    // are the rebuild stage's output (volume.build_octree) even though the
+    // renderer walks the brick map
+    const bool write_ref = true;
+    (void)flags;
     if (f->key_bytes == 4) {
         rc = sort_pairs<uint32_t>((const uint32_t *)f->keys, f->vals, (uint32_t *)f->keys_sorted,
                                   f->vals_sorted, f->n, f->key_bits, f->sort_ws, f->sort_ws_bytes,
@@ -121,7 +125,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         mark(3);
         rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
                                          f->n, write_ref ? f->left : nullptr, f->right, f->bmin,
-                                         f->bsize, f->nodes, f->leaves, f->winners, as.sigma,
+                                         f->bsize, nullptr, f->leaves, f->winners, as.sigma,
                                          f->rot_joint, nullptr, st);
     } else {
         rc = sort_pairs<u64>((const u64 *)f->keys, f->vals, (u64 *)f->keys_sorted, f->vals_sorted,
@@ -135,7 +139,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         mark(3);
         rc = launch_build_tree<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n,
                                     write_ref ? f->left : nullptr, f->right, f->bmin, f->bsize,
-                                    f->nodes, f->leaves, f->winners, as.sigma, f->rot_joint,
+                                    nullptr, f->leaves, f->winners, as.sigma, f->rot_joint,
                                     nullptr, st);
     }
     if (rc) return rc;
