@@ -21,20 +21,32 @@ __global__ void brick_heads_kernel(const K *__restrict__ codes, int64_t n_host,
     const bool ok = i < n;
     const u64 c = ok ? (u64)codes[i] : 0ull;
     const int x = (int)compact_bits3(c), y = (int)compact_bits3(c >> 1), z = (int)compact_bits3(c >> 2);
-    // leaf AABB: one atomic per warp and bound
-    const int lx = __reduce_min_sync(0xffffffffu, ok ? x : INT32_MAX);
-    const int ly = __reduce_min_sync(0xffffffffu, ok ? y : INT32_MAX);
-    const int lz = __reduce_min_sync(0xffffffffu, ok ? z : INT32_MAX);
-    const int hx = __reduce_max_sync(0xffffffffu, ok ? x + 1 : INT32_MIN);
-    const int hy = __reduce_max_sync(0xffffffffu, ok ? y + 1 : INT32_MIN);
-    const int hz = __reduce_max_sync(0xffffffffu, ok ? z + 1 : INT32_MIN);
-    if ((threadIdx.x & 31) == 0 && lx != INT32_MAX) {
-        atomicMin(aabb + 0, lx);
-        atomicMin(aabb + 1, ly);
-        atomicMin(aabb + 2, lz);
-        atomicMax(aabb + 3, hx);
-        atomicMax(aabb + 4, hy);
-        atomicMax(aabb + 5, hz);
+    // leaf AABB: warp reduce, block reduce in shared memory, one atomic per
+    // block and bound (global atomics on 6 words would serialise otherwise)
+    __shared__ int red[6][8];
+    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    int v[6] = {ok ? x : INT32_MAX, ok ? y : INT32_MAX, ok ? z : INT32_MAX,
+                ok ? x + 1 : INT32_MIN, ok ? y + 1 : INT32_MIN, ok ? z + 1 : INT32_MIN};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        v[k] = __reduce_min_sync(0xffffffffu, v[k]);
+        v[k + 3] = __reduce_max_sync(0xffffffffu, v[k + 3]);
+    }
+    if (ln == 0)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) red[k][wid] = v[k];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        int r = red[k][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            r = k < 3 ? min(r, red[k][w]) : max(r, red[k][w]);
+        if (k < 3 ? r != INT32_MAX : r != INT32_MIN) {
+            if (k < 3)
+                atomicMin(aabb + k, r);
+            else
+                atomicMax(aabb + k, r);
+        }
     }
     if (!ok) return;
     if (i > 0 && ((u64)codes[i - 1] >> 9) == (c >> 9)) return;

@@ -45,6 +45,9 @@ namespace artemis {
 #ifndef ARTEMIS_MIN_BLOCKS
 #define ARTEMIS_MIN_BLOCKS 4
 #endif
+#ifndef ARTEMIS_DEDUP
+#define ARTEMIS_DEDUP 1
+#endif
 namespace {
 constexpr int kRenderWarps = 4;
 constexpr int kRenderThreads = 32 * kRenderWarps;
@@ -761,32 +764,52 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         }
         ARTEMIS_PHASE(4);
         // ---- phase C: shade the visible queued leaves level by level (a ray
-        // has at most one leaf per level, so its features accumulate in order)
+        // has at most one leaf per level, so its features accumulate in order).
+        // Rays of a tile often hit the same leaf at the same level: lanes with
+        // equal FLUT rows are grouped (__match_any_sync) and the row is read
+        // once per group, then applied to every member ray.
         if (kMode != kCount) {
             __syncwarp();
+            uint32_t *wm = reinterpret_cast<uint32_t *>(wl + 32);  // group member masks
             for (int k = 0; k < kQCap; ++k) {
                 if (!__any_sync(0xffffffffu, nq > k)) break;
-                const bool vis = nq > k && q_val[k * kRenderThreads + tid].x > 0.0f;
-                const unsigned m = __ballot_sync(0xffffffffu, vis);
-                const int cnt = __popc(m);
-                if (vis) wl[__popc(m & lt)] = (uint16_t)lane;
+                const int qme = k * kRenderThreads + tid;
+                const bool vis = nq > k && q_val[qme].x > 0.0f;
+                const uint32_t key = vis ? (q_id[qme] & ~kDenseFlag) : (0x80000000u | (uint32_t)lane);
+#if ARTEMIS_DEDUP
+                const unsigned grpm = __match_any_sync(0xffffffffu, key);
+#else
+                const unsigned grpm = 1u << lane;
+                (void)key;
+#endif
+                const bool leader = vis && lane == __ffs(grpm) - 1;
+                const unsigned ml = __ballot_sync(0xffffffffu, leader);
+                const int cnt = __popc(ml);
+                if (leader) {
+                    const int slot = __popc(ml & lt);
+                    wl[slot] = (uint16_t)lane;
+                    wm[slot] = grpm;
+                }
                 __syncwarp();
                 for (int item = grp; item - grp < cnt; item += hpi) {
-                    if (item < cnt) {
-                        const int s = (int)wl[item];
-                        const int qi = k * kRenderThreads + wbase + s;
-                        const uint32_t bf = q_id[qi] & ~kDenseFlag;
-                        const float4 bv = q_val[qi];
-                        float Y[H];
-                        sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
-                        if (kVec) {
-                            const float4 *row = reinterpret_cast<const float4 *>(
-                                p.coef + (size_t)bf * p.coef_stride);
-                            float4 *dst = reinterpret_cast<float4 *>(feat + s * cp);
-                            for (int c4 = q; c4 < units; c4 += lph) {
-                                float4 v[H];
+                    if (item >= cnt) continue;
+                    const int s0 = (int)wl[item];
+                    unsigned members = wm[item];
+                    const uint32_t bf = q_id[k * kRenderThreads + wbase + s0] & ~kDenseFlag;
+                    if (kVec) {
+                        const float4 *row = reinterpret_cast<const float4 *>(
+                            p.coef + (size_t)bf * p.coef_stride);
+                        for (int c4 = q; c4 < units; c4 += lph) {
+                            float4 v[H];
 #pragma unroll
-                                for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
+                            for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
+                            unsigned mm = members;
+                            while (mm) {
+                                const int s = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                const float4 bv = q_val[k * kRenderThreads + wbase + s];
+                                float Y[H];
+                                sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
                                 float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
 #pragma unroll
                                 for (int h = 0; h < H; ++h) {
@@ -795,15 +818,23 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                                     az = fmaf(v[h].z, Y[h], az);
                                     aw = fmaf(v[h].w, Y[h], aw);
                                 }
-                                float4 f = dst[c4];
+                                float4 *dst = reinterpret_cast<float4 *>(feat + s * cp) + c4;
+                                float4 f = *dst;
                                 f.x += bv.x * ax;
                                 f.y += bv.x * ay;
                                 f.z += bv.x * az;
                                 f.w += bv.x * aw;
-                                dst[c4] = f;
+                                *dst = f;
                             }
-                        } else {
-                            const float *row = p.coef + (size_t)bf * p.coef_stride;
+                        }
+                    } else {
+                        const float *row = p.coef + (size_t)bf * p.coef_stride;
+                        while (members) {
+                            const int s = __ffs(members) - 1;
+                            members &= members - 1;
+                            const float4 bv = q_val[k * kRenderThreads + wbase + s];
+                            float Y[H];
+                            sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
                             for (int c = q; c < C; c += lph) {
                                 float acc_c = 0.0f;
 #pragma unroll

@@ -7,15 +7,12 @@ from paper_2202_05628_b200 import build_lib  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "s24q8": ("ARTEMIS_SMEM_STACK=24",),
-    "s24q6": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=64"),
-    "s24q6b4": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=64",
-                "ARTEMIS_MIN_BLOCKS=4"),
-    "s28q6b4": ("ARTEMIS_SMEM_STACK=28", "ARTEMIS_QCAP=6", "ARTEMIS_QTHRESH=64",
-                "ARTEMIS_MIN_BLOCKS=4"),
-    "s24q5b4": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=48",
-                "ARTEMIS_MIN_BLOCKS=4"),
-    "s24q8t96": ("ARTEMIS_SMEM_STACK=24", "ARTEMIS_QTHRESH=96"),
+    "nodedup": ("ARTEMIS_DEDUP=0",),
+    "q8t96": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=96", "ARTEMIS_MIN_BLOCKS=3"),
+    "q4t48": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48"),
+    "b3": ("ARTEMIS_MIN_BLOCKS=3",),
+    "t96": ("ARTEMIS_QTHRESH=96",),
+    "t32": ("ARTEMIS_QTHRESH=32",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
