@@ -50,7 +50,17 @@ __device__ __forceinline__ int brick_lookup(const BrickMap &bm, int bx, int by, 
 
 // Exact plane crossing fl((k - o) / d) -- the same double the reference's
 // slab test computes for the plane k of a unit cell.
+#ifdef ARTEMIS_PHASE_CLOCKS
+__device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick skips, syncs
+#define ARTEMIS_STAT(i) atomicAdd(&g_walk_stats[i], 1ull)
+#else
+#define ARTEMIS_STAT(i) \
+    do {                \
+    } while (0)
+#endif
+
 __device__ __forceinline__ double crossing(int k, double o, double d) {
+    ARTEMIS_STAT(0);
     return __ddiv_rn(__dadd_rn((double)k, -o), d);
 }
 
@@ -58,6 +68,7 @@ __device__ __forceinline__ double crossing(int k, double o, double d) {
 // from an estimate inside [cmin, cmax]; returns its exact entry/exit.
 __device__ __forceinline__ void sync_axis(double o, double d, double t, int cmin, int cmax,
                                           int &c, double &E, double &X) {
+    ARTEMIS_STAT(3);
     const double est = floor(o + t * d);
     c = est < (double)cmin ? cmin : est > (double)cmax ? cmax : (int)est;
     if (d > 0.0) {  // slab c = [cross(c), cross(c+1))

@@ -145,11 +145,13 @@ extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
     cudaMemcpyFromSymbol(out, g_phase_clocks, sizeof(unsigned long long) * 7);
     cudaMemcpyFromSymbol(out + 7, g_fallbacks, sizeof(unsigned long long));
     cudaMemcpyFromSymbol(out + 8, g_tests, sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out + 9, g_walk_stats, sizeof(unsigned long long) * 4);
     if (reset) {
         unsigned long long z[8] = {0};
         cudaMemcpyToSymbol(g_phase_clocks, z, sizeof(z));
         cudaMemcpyToSymbol(g_fallbacks, z, sizeof(unsigned long long));
         cudaMemcpyToSymbol(g_tests, z, sizeof(unsigned long long));
+        cudaMemcpyToSymbol(g_walk_stats, z, sizeof(unsigned long long) * 4);
     }
     return 0;
 }
@@ -351,7 +353,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     int cc[3] = {0, 0, 0}, cs[3] = {0, 0, 0};
     double cE[3] = {0, 0, 0}, cX[3] = {0, 0, 0};
     double t_end = 0.0;
-    int cb[3] = {INT32_MIN, 0, 0}, cbid = -1;
+    int cb[3] = {0, 0, 0}, cbid = -1;
+    double cTb[3] = {0, 0, 0};
     int aL[3] = {0, 0, 0}, aU[3] = {0, 0, 0};
     if (kDDA) {
 #pragma unroll
@@ -393,81 +396,50 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         ++nq;
         prefetch_l2(p.leaves + 2 * (size_t)leaf);
     };
-    // ---- exact cell walk (bricks.cuh)
-    auto walk_advance = [&]() {
-        const double tn = fmin(cX[0], fmin(cX[1], cX[2]));
-        if (!(tn < p.t_max) || !(tn < t_end)) {
-            walking = false;
-            return;
-        }
-        unsigned pend = (cX[0] == tn ? 1u : 0u) | (cX[1] == tn ? 2u : 0u) | (cX[2] == tn ? 4u : 0u);
-        while (pend) {
-            const int k = __ffs(pend) - 1;
-            pend &= pend - 1;
-            const int ck = (k == 0 ? cc[0] : k == 1 ? cc[1] : cc[2]) + (k == 0 ? cs[0] : k == 1 ? cs[1] : cs[2]);
-            const int lk = k == 0 ? aL[0] : k == 1 ? aL[1] : aL[2];
-            const int uk = k == 0 ? aU[0] : k == 1 ? aU[1] : aU[2];
-            if (ck < lk || ck >= uk) {
-                walking = false;
-                return;
-            }
-            const int sk = k == 0 ? cs[0] : k == 1 ? cs[1] : cs[2];
-            const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
-            const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
-            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk);
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-                if (a == k) {
-                    cc[a] = ck;
-                    cE[a] = tn;
-                    cX[a] = xn;
-                }
-        }
+    // ---- exact two-level walk (bricks.cuh): brick-level state (brick
+    // index, exact crossing of its exit plane per axis) is always valid; the
+    // cell-level state (cell, exact entry/exit crossing per axis) is valid
+    // while inside an occupied brick. Empty bricks cost one crossing each;
+    // entering an occupied brick re-derives the other axes' cells there.
+    auto brick_exit = [&](int a) {  // exact crossing of the current brick's exit plane on axis a
+        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a])
+                          : CUDART_INF;
     };
-    auto walk_skip_brick = [&]() {
-        double T[3], tb = CUDART_INF;
-        int P[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int b = cc[a] >> 3;
-            P[a] = cs[a] > 0 ? (b + 1) * 8 : b * 8;
-            T[a] = cs[a] != 0 ? crossing(P[a], og[a], dg[a]) : CUDART_INF;
-            tb = fmin(tb, T[a]);
-        }
-        if (!(tb < p.t_max) || !(tb < t_end)) {
-            walking = false;
-            return;
-        }
+    auto enter_brick = [&](unsigned advanced, double tn) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if (cs[a] == 0) continue;
-            if (T[a] == tb) {
-                const int cn = cs[a] > 0 ? P[a] : P[a] - 1;
-                if (cn < aL[a] || cn >= aU[a]) {
-                    walking = false;
-                    return;
-                }
+            if (advanced & (1u << a)) {
+                const int cn = cs[a] > 0 ? cb[a] * 8 : cb[a] * 8 + 7;
                 cc[a] = cn;
-                cE[a] = tb;
+                cE[a] = tn;
                 cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a]);
             } else {
-                const int b0 = (cc[a] >> 3) * 8;
-                sync_axis(og[a], dg[a], tb, max(b0, aL[a]), min(b0 + 7, aU[a] - 1), cc[a], cE[a],
-                          cX[a]);
+                sync_axis(og[a], dg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], cE[a], cX[a]);
             }
         }
     };
     auto walk_step = [&]() {
-        if (cb[0] != (cc[0] >> 3) || cb[1] != (cc[1] >> 3) || cb[2] != (cc[2] >> 3)) {
-            cb[0] = cc[0] >> 3;
-            cb[1] = cc[1] >> 3;
-            cb[2] = cc[2] >> 3;
+        if (cbid < 0) {  // empty brick: one brick step
+            ARTEMIS_STAT(2);
+            const double tn = fmin(cTb[0], fmin(cTb[1], cTb[2]));
+            if (!(tn < p.t_max) || !(tn < t_end)) {
+                walking = false;
+                return;
+            }
+            unsigned adv = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (cTb[a] == tn) {
+                    adv |= 1u << a;
+                    cb[a] += cs[a];
+                    cTb[a] = brick_exit(a);
+                }
             cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
-        }
-        if (cbid < 0) {
-            walk_skip_brick();
+            if (cbid >= 0) enter_brick(adv, tn);
             return;
         }
+        ARTEMIS_STAT(1);
         const double t0 = fmax(p.t_min, fmax(cE[0], fmax(cE[1], cE[2])));
         const double t1 = fmin(p.t_max, fmin(cX[0], fmin(cX[1], cX[2])));
         const uint32_t m = spread3_small(cc[0] & 7) | (spread3_small(cc[1] & 7) << 1) |
@@ -479,12 +451,38 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                                   (uint32_t)__popc(word & ((1u << (m & 31u)) - 1u));
             enqueue_hit(leaf, t0, t1);
         }
-        walk_advance();
+        // next cell: every axis whose exit crossing is the minimum steps
+        const double tn = fmin(cX[0], fmin(cX[1], cX[2]));
+        if (!(tn < p.t_max) || !(tn < t_end)) {
+            walking = false;
+            return;
+        }
+        unsigned pend = (cX[0] == tn ? 1u : 0u) | (cX[1] == tn ? 2u : 0u) | (cX[2] == tn ? 4u : 0u);
+        bool new_brick = false;
+        while (pend) {
+            const int k = __ffs(pend) - 1;
+            pend &= pend - 1;
+            const int sk = k == 0 ? cs[0] : k == 1 ? cs[1] : cs[2];
+            const int ck = (k == 0 ? cc[0] : k == 1 ? cc[1] : cc[2]) + sk;
+            const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
+            const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
+            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk);
+            const bool bchg = (ck >> 3) != (k == 0 ? cb[0] : k == 1 ? cb[1] : cb[2]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (a == k) {
+                    cc[a] = ck;
+                    cE[a] = tn;
+                    cX[a] = xn;
+                    if (bchg) {  // the cell exit just crossed was this brick's exit plane
+                        cb[a] = ck >> 3;
+                        cTb[a] = brick_exit(a);
+                    }
+                }
+            new_brick |= bchg;
+        }
+        if (new_brick) cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
     };
-    // one DFS step (_core.pyx:307-355 order) over a two-level record: test
-    // the (up to) four grandchild slots, order the hit ones as the binary
-    // DFS would (split-axis rule at the node, then inside each child), queue
-    // the leading leaves, push the rest in reverse so they pop in order.
     auto step = [&]() {
         if constexpr (kDDA) {
             walk_step();
@@ -629,8 +627,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                     cs[a] = dg[a] > 0.0 ? 1 : -1;
                     sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
                 }
+                cb[a] = cc[a] >> 3;
             }
-            cb[0] = INT32_MIN;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) cTb[a] = brick_exit(a);
+            cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
             walking = true;
         }
     };
