@@ -25,6 +25,7 @@ scaling). Rank 0 prints ONE JSON line. See DESIGN.md "Measurement".
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import math
 import os
@@ -57,6 +58,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--shard", default="frames", choices=["frames", "tiles"],
+                    help="N>1: frames (weak scaling, no collective) or 8x4 screen tiles of "
+                         "the same frame (strong scaling, one NCCL gather per frame)")
     return ap.parse_args()
 
 
@@ -232,6 +236,10 @@ def main():
     n_frames = args.warmup + args.steps
     sc = make_scene(args.config, max(64, n_frames * world) if args.config == "c2" else n_frames)
     frames = [(rank + world * s) % len(sc.poses) for s in range(n_frames)]
+    tiles = args.shard == "tiles" and world > 1
+    if tiles:  # every rank renders the same frame sequence, its own tiles
+        frames = [s % len(sc.poses) for s in range(n_frames)]
+        from paper_2202_05628_b200 import parallel as PL
     tables = {f: KM.pose_tables(sc.rig, KM.PoseSpec.make(sc.poses[f])) for f in set(frames)}
     fp = FramePipeline.from_scene(sc)
     cams = {f: fp.camera(sc.cameras[f][0]) for f in set(frames)}
@@ -241,9 +249,13 @@ def main():
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
 
     def frame(f, graph=True):
-        return fp.run(KM.PoseSpec.make(sc.poses[f]), cams[f],
-                      lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep, graph=graph,
-                      tables=tables[f])
+        out = fp.run(KM.PoseSpec.make(sc.poses[f]), cams[f],
+                     lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep, graph=graph,
+                     tables=tables[f], tiles=(rank, world) if tiles else None)
+        if tiles:
+            with torch.cuda.stream(stream):
+                PL.assemble_tiles(*out, W, H, dst=0)
+        return out
 
     for s in range(args.warmup):
         frame(frames[s])
@@ -272,7 +284,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = world * args.steps * rays / (total_ms / 1e3)
+    value = (1 if tiles else world) * args.steps * rays / (total_ms / 1e3)
 
     # ---- stage breakdown (eager, profiled) -> roofline of the render kernel
     fp.profile(True)
@@ -314,26 +326,20 @@ def main():
 
     # ---- e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
-        F, A, D = fp.outputs(W, H)
-        hF = torch.empty(F.shape, dtype=F.dtype, pin_memory=True)
-        hA = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
-        hD = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
-        h2d = sc.rig.n_joints * 21 * 8 + 200
-        d2h = hF.numel() * 4 + hA.numel() * 4 + hD.numel() * 4
-        e2e_steps = min(args.steps, 10)
+    if not args.no_e2e and not tiles:
+        h2d = sc.rig.n_joints * 21 * 8 + C.sizeof(cams[frames[0]])
+        d2h = rays * (sc.channels + 2) * 4
+        e2e_steps = args.steps
+        items = [(KM.PoseSpec.make(sc.poses[f]), sc.cameras[f][0])
+                 for f in frames[args.warmup:args.warmup + e2e_steps]]
+        for _ in fp.run_stream(items[:2], lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep):
+            pass  # warm the double-buffered graphs
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for s in range(e2e_steps):
-            f = frames[args.warmup + s]
-            pose = KM.PoseSpec.make(sc.poses[f])
-            F, A, D = fp.run(pose, sc.cameras[f][0], lambda_th=sc.lambda_th,
-                             sigma_dep=sc.sigma_dep)  # host FK + camera inside
-            with torch.cuda.stream(stream):
-                hF.copy_(F, non_blocking=True)
-                hA.copy_(A, non_blocking=True)
-                hD.copy_(D, non_blocking=True)
-            stream.synchronize()
+        # public API: host FK + pinned H2D of pose/camera + frame + D2H of
+        # F/alpha/depth into pinned host memory, every frame
+        for hF, hA, hD in fp.run_stream(items, lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep):
+            pass
         e2e_s = time.perf_counter() - t0
         e2e = {"value": world * e2e_steps * rays / e2e_s, "unit": "rays/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -351,12 +357,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "higher_is_better": True, "scaling": "strong" if tiles else "weak",
+            "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "image": [W, H], "rays_per_frame": rays,
                        "voxels": sc.n_voxels, "live_leaves": n_live, "in_bounds": n_in,
                        "channels": sc.channels, "sh_degree": sc.degree,
-                       "frames_per_rank": args.steps, "parallelism": f"frames-sharded x{world}",
+                       "frames_per_rank": args.steps,
+                       "parallelism": (f"tiles-sharded x{world} (8x4 tiles t % {world}, one "
+                                       f"NCCL gather per frame)" if tiles
+                                       else f"frames-sharded x{world}"),
                        "l2": "flushed between timed frames (256 MB write)",
                        "graph": True, "hit_rays": hit_rays, "hits": total_hits,
                        "unique_rows": unique_rows},

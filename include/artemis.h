@@ -252,9 +252,12 @@ int artemis_frame_destroy(artemis_frame frame);
 
 /* Per-frame inputs are HOST pointers: joint_aff (J,12) fp64 (rows 0..2 of
  * the per-joint delta matrices, rigging.py:343-345), rot_inv (J,3,3) fp64
- * (rigging.py:347) and the camera. They are copied into a device parameter
- * block ahead of the frame, so a captured graph replays unchanged for any
- * pose and camera of the same image size. joint_aff == NULL renders the
+ * (rigging.py:347) and the camera. They are staged in pinned host memory (a
+ * ring of 4 blocks) and copied asynchronously into a device parameter block
+ * ahead of the frame, so a captured graph replays unchanged for any pose and
+ * camera of the same image size. Up to 4 graphs are cached per handle
+ * (keyed by image size, flags and output pointers), so callers may rotate
+ * output buffers to overlap a frame's D2H read with the next frame. joint_aff == NULL renders the
  * canonical cells (identity warp, render.py:162-167).
  * flags: bit0 early stop, bit1 capture/replay a CUDA graph (needs a
  * non-default stream); bit2 is accepted for compatibility (the reference
@@ -289,6 +292,23 @@ int artemis_frame_get_tree(artemis_frame frame, artemis_frame_tree *out);
  * render of the last such run (synchronises on its last event). */
 int artemis_frame_profile(artemis_frame frame, int enable);
 int artemis_frame_stage_ms(artemis_frame frame, float *ms);
+
+/* ---- Multi-GPU tile shards ----------------------
+ * With tile sharding (artemis_camera tile_start/tile_stride) each rank packs
+ * the pixels of its 8x4 tiles into one contiguous shard -- tile-major, 32
+ * pixels per tile in tile-row order, (C + 2) floats per pixel: F[0..C),
+ * alpha, depth -- so a single gather moves only rendered pixels; the root
+ * unpacks every rank's shard into the full image. Replaces nothing in the
+ * reference (its render is single-process, render.py:322-363); the
+ * assembled image equals a single-GPU render bit for bit. */
+int64_t artemis_tiles_shard_floats(int width, int height, int channels, int tile_start,
+                                   int tile_stride);
+int artemis_tiles_pack(const float *F, const float *alpha, const float *depth, int width,
+                       int height, int channels, int tile_start, int tile_stride, float *packed,
+                       artemis_stream stream);
+int artemis_tiles_unpack(const float *packed, int width, int height, int channels,
+                         int tile_start, int tile_stride, float *F, float *alpha, float *depth,
+                         artemis_stream stream);
 
 /* Synchronous device -> host copy (parity helpers). */
 int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);

@@ -62,13 +62,26 @@ struct artemis_frame_s {
     void *sort_ws = nullptr, *resolve_ws = nullptr;
     size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
     FrameParams *params = nullptr;
-    // captured graph and the launch shape it was captured for
-    cudaGraphExec_t exec = nullptr;
-    int g_w = 0, g_h = 0, g_flags = 0, g_identity = -1, g_nj = 0;
-    const void *g_F = nullptr, *g_A = nullptr, *g_D = nullptr;
-    cudaStream_t g_stream = nullptr;
-    double g_lambda = 0, g_sigma_dep = 0;
-    int g_sharded = 0;
+    // pinned host staging for the per-frame inputs (a ring, so a frame's
+    // H2D copy never races the host filling the next frame's block)
+    static constexpr int kStaging = 4;
+    FrameParams *staging = nullptr;
+    cudaEvent_t staged[kStaging] = {nullptr, nullptr, nullptr, nullptr};
+    int stage_next = 0;
+    // captured graphs and the launch shape each was captured for: a few are
+    // kept so callers can rotate output buffers (double-buffered D2H)
+    // without re-capturing
+    struct GraphSlot {
+        cudaGraphExec_t exec = nullptr;
+        int w = 0, h = 0, flags = 0, identity = -1, nj = 0, sharded = 0;
+        const void *F = nullptr, *A = nullptr, *D = nullptr;
+        cudaStream_t stream = nullptr;
+        double lambda = 0, sigma_dep = 0;
+        unsigned long long used = 0;
+    };
+    static constexpr int kGraphSlots = 4;
+    GraphSlot graphs[kGraphSlots];
+    unsigned long long graph_clock = 0;
     int launches = 0;
     // stage profiling (eager runs only): events before warp, sort, resolve,
     // build, render and after render
@@ -224,6 +237,16 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->sort_ws, f->sort_ws_bytes);
     rc = rc ? rc : dev_alloc(&f->resolve_ws, f->resolve_ws_bytes);
     rc = rc ? rc : dev_alloc(&f->params, sizeof(FrameParams));
+    if (!rc) {
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void **>(&f->staging),
+                                       sizeof(FrameParams) * artemis_frame_s::kStaging);
+        for (int k = 0; e == cudaSuccess && k < artemis_frame_s::kStaging; ++k)
+            e = cudaEventCreateWithFlags(&f->staged[k], cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            set_cuda_error(e);
+            rc = ARTEMIS_ERR_OOM;
+        }
+    }
     if (rc) {
         artemis_frame_destroy(f);
         return rc;
@@ -234,9 +257,13 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
 
 extern "C" int artemis_frame_destroy(artemis_frame f) {
     if (!f) return ARTEMIS_OK;
-    if (f->exec) cudaGraphExecDestroy(f->exec);
+    for (auto &g : f->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     for (cudaEvent_t e : f->ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : f->staged)
+        if (e) cudaEventDestroy(e);
+    if (f->staging) cudaFreeHost(f->staging);
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
                     f->leaves, f->btable, f->brecs, f->bmeta,
@@ -257,32 +284,50 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
     if (!identity && (!rot_inv || n_joints < 1 || n_joints > f->asset.max_joints))
         return ARTEMIS_ERR_ARG;
     cudaStream_t st = S(stream);
-    // parameter block: camera + joint tables (host -> device, before the graph)
-    ARTEMIS_TRY(cudaMemcpyAsync(&f->params->cam, cam, sizeof(artemis_camera),
+    // parameter block: camera + joint tables, staged in pinned host memory and
+    // copied host -> device ahead of the graph on the frame's stream
+    const int sidx = f->stage_next;
+    f->stage_next = (sidx + 1) % artemis_frame_s::kStaging;
+    FrameParams *hp = f->staging + sidx;
+    ARTEMIS_TRY(cudaEventSynchronize(f->staged[sidx]));  // its last copy has completed
+    hp->cam = *cam;
+    ARTEMIS_TRY(cudaMemcpyAsync(&f->params->cam, &hp->cam, sizeof(artemis_camera),
                                 cudaMemcpyHostToDevice, st));
     if (identity) {
         static const double eye[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, eye, sizeof(eye), cudaMemcpyHostToDevice, st));
+        memcpy(hp->rot_inv, eye, sizeof(eye));
+        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, hp->rot_inv, sizeof(eye),
+                                    cudaMemcpyHostToDevice, st));
     } else {
-        ARTEMIS_TRY(cudaMemcpyAsync(f->params->aff, joint_aff, sizeof(double) * 12 * n_joints,
+        memcpy(hp->aff, joint_aff, sizeof(double) * 12 * n_joints);
+        memcpy(hp->rot_inv, rot_inv, sizeof(double) * 9 * n_joints);
+        ARTEMIS_TRY(cudaMemcpyAsync(f->params->aff, hp->aff, sizeof(double) * 12 * n_joints,
                                     cudaMemcpyHostToDevice, st));
-        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, rot_inv, sizeof(double) * 9 * n_joints,
-                                    cudaMemcpyHostToDevice, st));
+        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, hp->rot_inv,
+                                    sizeof(double) * 9 * n_joints, cudaMemcpyHostToDevice, st));
     }
+    ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));
     const int sharded = cam->tile_stride > 1;
     const int use_graph = (flags & 2) && st != nullptr;
     if (!use_graph)
         return enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded, lambda_th,
                              sigma_dep, flags, F, alpha, depth, st);
-    const bool same = f->exec && f->g_w == cam->width && f->g_h == cam->height &&
-                      f->g_flags == flags && f->g_identity == identity && f->g_nj == n_joints &&
-                      f->g_F == F && f->g_A == alpha && f->g_D == depth && f->g_stream == st &&
-                      f->g_lambda == lambda_th && f->g_sigma_dep == sigma_dep &&
-                      f->g_sharded == sharded;
-    if (!same) {
-        if (f->exec) {
-            cudaGraphExecDestroy(f->exec);
-            f->exec = nullptr;
+    artemis_frame_s::GraphSlot *slot = nullptr, *victim = &f->graphs[0];
+    for (auto &g : f->graphs) {
+        if (g.exec && g.w == cam->width && g.h == cam->height && g.flags == flags &&
+            g.identity == identity && g.nj == n_joints && g.F == F && g.A == alpha &&
+            g.D == depth && g.stream == st && g.lambda == lambda_th &&
+            g.sigma_dep == sigma_dep && g.sharded == sharded) {
+            slot = &g;
+            break;
+        }
+        if (!g.exec || (victim->exec && g.used < victim->used)) victim = &g;
+    }
+    if (!slot) {
+        slot = victim;
+        if (slot->exec) {
+            cudaGraphExecDestroy(slot->exec);
+            slot->exec = nullptr;
         }
         ARTEMIS_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         int rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded,
@@ -297,27 +342,28 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
             set_cuda_error(e);
             return ARTEMIS_ERR_CUDA;
         }
-        e = cudaGraphInstantiate(&f->exec, g, 0);
+        e = cudaGraphInstantiate(&slot->exec, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) {
             set_cuda_error(e);
-            f->exec = nullptr;
+            slot->exec = nullptr;
             return ARTEMIS_ERR_CUDA;
         }
-        f->g_w = cam->width;
-        f->g_h = cam->height;
-        f->g_flags = flags;
-        f->g_identity = identity;
-        f->g_nj = n_joints;
-        f->g_F = F;
-        f->g_A = alpha;
-        f->g_D = depth;
-        f->g_stream = st;
-        f->g_lambda = lambda_th;
-        f->g_sigma_dep = sigma_dep;
-        f->g_sharded = sharded;
+        slot->w = cam->width;
+        slot->h = cam->height;
+        slot->flags = flags;
+        slot->identity = identity;
+        slot->nj = n_joints;
+        slot->F = F;
+        slot->A = alpha;
+        slot->D = depth;
+        slot->stream = st;
+        slot->lambda = lambda_th;
+        slot->sigma_dep = sigma_dep;
+        slot->sharded = sharded;
     }
-    ARTEMIS_TRY(cudaGraphLaunch(f->exec, st));
+    slot->used = ++f->graph_clock;
+    ARTEMIS_TRY(cudaGraphLaunch(slot->exec, st));
     return ARTEMIS_OK;
 }
 

@@ -144,6 +144,50 @@ class FramePipeline:
             cur.wait_stream(self.stream)  # consumers on the caller's stream see the frame
         return F, A, D
 
+    def run_stream(self, items, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
+                   early_stop: bool = True, buffers: int = 2):
+        """Render a sequence of (pose, camera) frames to HOST memory.
+
+        Yields (F, alpha, depth) as pinned host tensors, one triple per item,
+        in order. Frame k+1 renders while frame k's result is copied
+        device -> host on a separate copy stream (double-buffered device and
+        pinned host outputs), so the sequence runs at max(render, D2H) per
+        frame rather than their sum. A yielded triple stays valid until the
+        generator is advanced `buffers - 1` more times."""
+        copy_stream = torch.cuda.Stream()
+        dev, host, done, copied = [], [], [], []
+        pending = []
+        for k, (pose, camera) in enumerate(items):
+            cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
+            n = cam.width * cam.height
+            b = k % buffers
+            if len(dev) <= b:
+                with torch.cuda.stream(self.stream):
+                    dev.append((empty((n, self.channels), np.float32), empty(n, np.float32),
+                                empty(n, np.float32)))
+                host.append(tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                                  for t in dev[b]))
+                done.append(torch.cuda.Event())
+                copied.append(torch.cuda.Event())
+            else:
+                self.stream.wait_event(copied[b])  # device buffer b has been read out
+            self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                     early_stop=early_stop, out=dev[b])
+            done[b].record(self.stream)
+            copy_stream.wait_event(done[b])
+            with torch.cuda.stream(copy_stream):
+                for h, d in zip(host[b], dev[b]):
+                    h.copy_(d, non_blocking=True)
+            copied[b].record(copy_stream)
+            pending.append(b)
+            if len(pending) > 1:
+                p = pending.pop(0)
+                copied[p].synchronize()
+                yield host[p]
+        for p in pending:
+            copied[p].synchronize()
+            yield host[p]
+
     def counts(self):
         n_in, n_live = C.c_int64(), C.c_int64()
         check(_lib.lib().artemis_frame_counts(self._h, C.byref(n_in), C.byref(n_live),

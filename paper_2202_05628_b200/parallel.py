@@ -6,16 +6,19 @@ shards without any exchange inside a frame:
 
 * frames  (configs[3], configs[4]): each rank warps, rebuilds and renders
           its own frames -- weak scaling, no data-path collective;
+* views   (configs[1]): view v on rank v % world, same as frames;
 * tiles   (configs[2]): every rank rebuilds the same posed tree and renders
-          the 8x4-pixel tiles t with t % world == rank; one reduction then
-          assembles the image on the root: F and alpha are SUM-reduced
-          (other ranks' pixels are exactly 0) and depth MIN-reduced (other
-          ranks' pixels are +inf), so the assembled frame is bit-identical
-          to a single-GPU render.
+          the 8x4-pixel tiles t with t % world == rank; each rank packs only
+          those pixels into one contiguous shard (artemis_tiles_pack), ONE
+          gather moves the shards to the root, and the root unpacks them
+          into the image (artemis_tiles_unpack). Only rendered pixels cross
+          NVLink ((world-1)/world of the frame), and the assembled frame is
+          bit-identical to a single-GPU render.
 """
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -27,7 +30,7 @@ def world() -> tuple[int, int]:
 
 
 def shard_frames(n_frames: int, rank: int, world_size: int) -> list[int]:
-    """Round-robin frame ownership (frame f on rank f % world)."""
+    """Round-robin frame (or view) ownership: frame f on rank f % world."""
     return [f for f in range(n_frames) if f % world_size == rank]
 
 
@@ -45,15 +48,73 @@ def tile_shard(rank: int, world_size: int) -> tuple[int, int]:
     return (rank, world_size) if world_size > 1 else (0, 1)
 
 
-def assemble_tiles(F: torch.Tensor, alpha: torch.Tensor, depth: torch.Tensor, dst: int = 0):
-    """Combine tile-sharded partial frames onto `dst` in place (one
-    reduction per buffer; exact because the shards are disjoint)."""
+def n_tiles(width: int, height: int) -> int:
+    return ((width + 7) // 8) * ((height + 3) // 4)
+
+
+def shard_floats(width: int, height: int, channels: int, start: int, stride: int) -> int:
+    """Floats in one packed shard (artemis_tiles_shard_floats)."""
+    t = n_tiles(width, height)
+    return (max(0, (t - start + stride - 1) // stride) if start < t else 0) * 32 * (channels + 2)
+
+
+def tile_pixels(width: int, height: int, start: int, stride: int) -> np.ndarray:
+    """Host statement of the shard layout: pixel index (row-major) of every
+    packed slot, -1 for slots outside the image. Slot s of the shard is
+    pixel (s & 31) of tile start + (s >> 5) * stride, tile-row order."""
+    tx = (width + 7) // 8
+    t = np.arange(start, n_tiles(width, height), stride, dtype=np.int64)
+    s = np.arange(32, dtype=np.int64)
+    px = (t[:, None] % tx) * 8 + (s[None, :] & 7)
+    py = (t[:, None] // tx) * 4 + (s[None, :] >> 3)
+    pix = py * width + px
+    return np.where((px < width) & (py < height), pix, -1).reshape(-1)
+
+
+def gather_shards(packed: torch.Tensor, sizes: list[int], dst: int = 0):
+    """ONE gather of every rank's packed shard to `dst` (shards padded to the
+    largest size). Returns the list of per-rank shards on dst, None elsewhere."""
+    rank, ws = world()
+    cap = max(sizes)
+    if packed.numel() < cap:
+        buf = torch.zeros(cap, dtype=packed.dtype, device=packed.device)
+        buf[:packed.numel()] = packed
+    else:
+        buf = packed
+    gl = [torch.empty_like(buf) for _ in range(ws)] if rank == dst else None
+    dist.gather(buf, gather_list=gl, dst=dst)
+    if rank != dst:
+        return None
+    return [g[:sizes[r]] for r, g in enumerate(gl)]
+
+
+def assemble_tiles(F: torch.Tensor, alpha: torch.Tensor, depth: torch.Tensor, width: int,
+                   height: int, dst: int = 0):
+    """Assemble a tile-sharded frame on `dst` in place: every rank's F/alpha/
+    depth holds its own tiles (render with tiles=tile_shard(rank, world));
+    on return dst's buffers hold the whole image. Device tensors (CUDA)."""
+    from . import _lib
+    from ._lib import check
+    from .device import ptr
+
     rank, ws = world()
     if ws == 1:
         return F, alpha, depth
-    dist.reduce(F, dst=dst, op=dist.ReduceOp.SUM)
-    dist.reduce(alpha, dst=dst, op=dist.ReduceOp.SUM)
-    dist.reduce(depth, dst=dst, op=dist.ReduceOp.MIN)
+    L = _lib.lib()
+    C = F.numel() // (width * height)
+    st = torch.cuda.current_stream().cuda_stream or None
+    sizes = [shard_floats(width, height, C, r, ws) for r in range(ws)]
+    packed = torch.empty(max(sizes[rank], 1), dtype=torch.float32, device=F.device)
+    if sizes[rank]:
+        check(L.artemis_tiles_pack(ptr(F), ptr(alpha), ptr(depth), width, height, C, rank, ws,
+                                   ptr(packed), st), "tiles_pack")
+    shards = gather_shards(packed[:sizes[rank]], sizes, dst)
+    if rank == dst:
+        for r, sh in enumerate(shards):
+            if r == dst or not sizes[r]:
+                continue
+            check(L.artemis_tiles_unpack(ptr(sh), width, height, C, r, ws, ptr(F), ptr(alpha),
+                                         ptr(depth), st), "tiles_unpack")
     return F, alpha, depth
 
 

@@ -1,0 +1,5 @@
+cd "$GRAFT_REPO_ROOT"
+ARTEMIS_LIB_PATH=$PWD/variants/libartemis_clocks.so timeout 300 python scripts/phase_clocks.py 2>&1 | tail -3
+for v in nodedup; do
+ARTEMIS_LIB_PATH=$PWD/variants/libartemis_$v.so timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['ms_per_step'], d['stage_ms']['render'])"
+done

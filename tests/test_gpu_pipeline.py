@@ -310,3 +310,47 @@ class TestTileSharding:
         assert np.array_equal(As, A.cpu().numpy())
         assert np.array_equal(Ds, D.cpu().numpy())
         fp.close()
+
+
+class TestTileGather:
+    def test_pack_matches_host_layout_and_unpack_assembles(self, mini):
+        """artemis_tiles_pack writes exactly the layout parallel.tile_pixels
+        states; unpacking every rank's shard into one image reproduces the
+        unsharded frame bit for bit (ranks simulated one after another)."""
+        from paper_2202_05628_b200 import _lib
+        from paper_2202_05628_b200 import parallel as PL
+        from paper_2202_05628_b200.device import ptr
+        from paper_2202_05628_b200.frame import FramePipeline
+
+        L = _lib.lib()
+        fp = FramePipeline.from_scene(mini)
+        pose = KM.PoseSpec.make(mini.poses[0])
+        cam = mini.cameras[0][0]
+        W, H, C_ = cam.width, cam.height, mini.channels
+        F, A, D = [x.clone() for x in fp.run(pose, cam, graph=False)]
+        fp.stream.synchronize()
+        full = np.concatenate([F.cpu().numpy(), A.cpu().numpy()[:, None],
+                               D.cpu().numpy()[:, None]], axis=1)
+        world = 3
+        Fo = torch.full_like(F, -7.0)
+        Ao = torch.full_like(A, -7.0)
+        Do = torch.full_like(D, -7.0)
+        st = torch.cuda.current_stream().cuda_stream
+        for r in range(world):
+            Fr, Ar, Dr = [x.clone() for x in fp.run(pose, cam, graph=False, tiles=(r, world))]
+            torch.cuda.synchronize()
+            n = L.artemis_tiles_shard_floats(W, H, C_, r, world)
+            assert n == PL.shard_floats(W, H, C_, r, world)
+            packed = torch.empty(n, dtype=torch.float32, device="cuda")
+            assert L.artemis_tiles_pack(ptr(Fr), ptr(Ar), ptr(Dr), W, H, C_, r, world,
+                                        ptr(packed), st) == 0
+            pix = PL.tile_pixels(W, H, r, world)
+            want = np.where(pix[:, None] >= 0, full[np.maximum(pix, 0)], 0.0)
+            assert np.array_equal(packed.cpu().numpy().reshape(-1, C_ + 2), want)
+            assert L.artemis_tiles_unpack(ptr(packed), W, H, C_, r, world, ptr(Fo), ptr(Ao),
+                                          ptr(Do), st) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(Fo.cpu().numpy(), F.cpu().numpy())
+        assert np.array_equal(Ao.cpu().numpy(), A.cpu().numpy())
+        assert np.array_equal(Do.cpu().numpy(), D.cpu().numpy())
+        fp.close()
