@@ -193,6 +193,25 @@ int artemis_forward_fit(const artemis_tree_view *tree, const artemis_shading *sh
                         double *hit_t0, double *hit_t1, float *F, double *alpha,
                         artemis_stream stream);
 
+/* ---- Training gradients ----------------------------------------------
+ * replaces animvox/_core.pyx:661-755 backward_rays (fit.py:108-146
+ * backward_batch). The CSR trace of artemis_forward_fit / forward_fit
+ * (offsets (R+1) int64, hit_idx/t0/t1 (M)), unit world directions (R,3),
+ * rot tables, the FLUT (n_flut, width) and dL/dF (R,C), dL/dalpha (R) in
+ * the same real type (real_bytes 4 = float, 8 = double, as the reference's
+ * fused real_t) -> grad (n_flut, width) of that type, zero for untouched
+ * rows. Accumulation is deterministic (each grad entry summed in ascending
+ * ray order, the reference's deterministic schedule) for either value of
+ * `deterministic`. Workspace: artemis_backward_workspace_bytes. */
+size_t artemis_backward_workspace_bytes(int64_t n_hits, int64_t n_flut);
+int artemis_backward_rays(const int64_t *offsets, int64_t n_rays, const int64_t *hit_idx,
+                          const double *hit_t0, const double *hit_t1, int64_t n_hits,
+                          const double *dirs_w, const int32_t *rot_index, const double *rot_inv,
+                          const void *flut, int64_t n_flut, int width, const void *dldf,
+                          const void *dlda, int real_bytes, int degree, int channels,
+                          int deterministic, void *grad, void *workspace,
+                          size_t workspace_bytes, artemis_stream stream);
+
 /* Device ray generation (parity helper for rays_for_camera + _grid_rays).
  * og/dg/dw: (W*H, 3) fp64, row-major pixels. */
 int artemis_camera_rays(const artemis_camera *cam /* host */, double *og, double *dg,

@@ -98,6 +98,9 @@ _SIGS = {
     "artemis_brickmap_bytes": (SZ, [I64, P]),
     "artemis_brickmap_build": (INT, [P, I64, P, P, P, SZ, C.POINTER(BrickMap), P]),
     "artemis_frame_stage_ms": (INT, [P, C.POINTER(C.c_float)]),
+    "artemis_backward_workspace_bytes": (SZ, [I64, I64]),
+    "artemis_backward_rays": (INT, [P, I64, P, P, P, I64, P, P, P, P, I64, INT, P, P, INT, INT,
+                                    INT, INT, P, P, SZ, P]),
     "artemis_tiles_shard_floats": (I64, [INT, INT, INT, INT, INT]),
     "artemis_tiles_pack": (INT, [P, P, P, INT, INT, INT, INT, INT, P, P]),
     "artemis_tiles_unpack": (INT, [P, INT, INT, INT, INT, INT, P, P, P, P]),

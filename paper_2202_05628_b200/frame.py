@@ -154,39 +154,42 @@ class FramePipeline:
         pinned host outputs), so the sequence runs at max(render, D2H) per
         frame rather than their sum. A yielded triple stays valid until the
         generator is advanced `buffers - 1` more times."""
-        copy_stream = torch.cuda.Stream()
-        dev, host, done, copied = [], [], [], []
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream()
+            self._stream_bufs = {}
+        copy_stream = self._copy_stream
         pending = []
         for k, (pose, camera) in enumerate(items):
             cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
             n = cam.width * cam.height
             b = k % buffers
-            if len(dev) <= b:
+            # device + pinned host buffers persist across calls (allocation
+            # and graph capture happen once per image size)
+            key = (cam.width, cam.height, b)
+            if key not in self._stream_bufs:
                 with torch.cuda.stream(self.stream):
-                    dev.append((empty((n, self.channels), np.float32), empty(n, np.float32),
-                                empty(n, np.float32)))
-                host.append(tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-                                  for t in dev[b]))
-                done.append(torch.cuda.Event())
-                copied.append(torch.cuda.Event())
-            else:
-                self.stream.wait_event(copied[b])  # device buffer b has been read out
+                    d = (empty((n, self.channels), np.float32), empty(n, np.float32),
+                         empty(n, np.float32))
+                h = tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in d)
+                self._stream_bufs[key] = (d, h, torch.cuda.Event(), torch.cuda.Event())
+            dev_b, host_b, done_b, copied_b = self._stream_bufs[key]
+            self.stream.wait_event(copied_b)  # device buffer b has been read out
             self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
-                     early_stop=early_stop, out=dev[b])
-            done[b].record(self.stream)
-            copy_stream.wait_event(done[b])
+                     early_stop=early_stop, out=dev_b)
+            done_b.record(self.stream)
+            copy_stream.wait_event(done_b)
             with torch.cuda.stream(copy_stream):
-                for h, d in zip(host[b], dev[b]):
+                for h, d in zip(host_b, dev_b):
                     h.copy_(d, non_blocking=True)
-            copied[b].record(copy_stream)
-            pending.append(b)
+            copied_b.record(copy_stream)
+            pending.append((host_b, copied_b))
             if len(pending) > 1:
-                p = pending.pop(0)
-                copied[p].synchronize()
-                yield host[p]
-        for p in pending:
-            copied[p].synchronize()
-            yield host[p]
+                h, ev = pending.pop(0)
+                ev.synchronize()
+                yield h
+        for h, ev in pending:
+            ev.synchronize()
+            yield h
 
     def counts(self):
         n_in, n_live = C.c_int64(), C.c_int64()

@@ -13,8 +13,7 @@ arrays in the reference's dtypes:
   forward_fit    :562-655
 
 ``nthreads`` is accepted and ignored (results never depended on it).
-``backward_rays`` (training) is not on the
-frame path and is not provided by this module yet.
+  backward_rays  :661-755 (training gradients)
 """
 
 from __future__ import annotations
@@ -339,7 +338,47 @@ def camera_struct(R, origin, fx, fy, cx, cy, width, height, lo, cell) -> _lib.Ca
     return cam
 
 
-def backward_rays(*args, **kwargs):
-    raise NotImplementedError(
-        "backward_rays (training gradients, animvox/_core.pyx:661-755) is the next row of "
-        "SURVEY.md section 8f and is not provided by the B200 frame path yet")
+def backward_rays_device(offsets, hit_idx, hit_t0, hit_t1, dirs_w, rot_index, rot_inv, flut,
+                         dldf, dlda, degree, channels, deterministic=True):
+    """Device tensors in, device grad (n_flut, width) out; real type of flut."""
+    L = _lib.lib()
+    n_flut, width = int(flut.shape[0]), int(flut.shape[1])
+    n_rays = int(offsets.numel()) - 1
+    n_hits = int(hit_idx.numel())
+    grad = torch.empty_like(flut)
+    ws = workspace(L.artemis_backward_workspace_bytes(n_hits, n_flut))
+    check(L.artemis_backward_rays(ptr(offsets), n_rays, ptr(hit_idx), ptr(hit_t0), ptr(hit_t1),
+                                  n_hits, ptr(dirs_w), ptr(rot_index), ptr(rot_inv), ptr(flut),
+                                  n_flut, width, ptr(dldf), ptr(dlda), flut.element_size(),
+                                  int(degree), int(channels), int(bool(deterministic)),
+                                  ptr(grad), ptr(ws), ws.numel(), stream_handle()),
+          "backward_rays")
+    return grad
+
+
+def backward_rays(offsets, hit_idx, hit_t0, hit_t1, dirs_w, rot_index, rot_inv, flut, dldf, dlda,
+                  degree, channels, deterministic=True, nthreads=1):
+    """_core.pyx:661-755: gradient of the batch loss w.r.t. every FLUT entry
+    (float32 instantiation when flut is float32, else float64); dldf/dlda are
+    taken in flut's real type, as the reference's fused real_t requires."""
+    fl = np.asarray(flut)
+    rdt = np.float32 if fl.dtype == np.float32 else np.float64
+    if fl.ndim != 2:
+        raise ValueError("flut must be (N, H*C+1)")
+    h = (int(degree) + 1) ** 2
+    if fl.shape[1] != h * int(channels) + 1:
+        raise ValueError("flut width must be (degree+1)^2 * channels + 1")
+    off = np.ascontiguousarray(offsets, dtype=np.int64).reshape(-1)
+    hi = np.ascontiguousarray(hit_idx, dtype=np.int64).reshape(-1)
+    if hi.size == 0 or off.size <= 1 or int(np.diff(off).max(initial=0)) == 0:
+        return np.zeros(fl.shape, dtype=rdt)
+    g = backward_rays_device(
+        upload(off, np.int64), upload(hi, np.int64),
+        upload(np.asarray(hit_t0).reshape(-1), np.float64),
+        upload(np.asarray(hit_t1).reshape(-1), np.float64),
+        upload(np.asarray(dirs_w).reshape(-1, 3), np.float64),
+        upload(np.asarray(rot_index).reshape(-1), np.int32),
+        upload(np.asarray(rot_inv).reshape(-1, 9), np.float64),
+        upload(fl, rdt), upload(np.asarray(dldf).reshape(-1, int(channels)), rdt),
+        upload(np.asarray(dlda).reshape(-1), rdt), degree, channels, deterministic)
+    return download(g)

@@ -44,3 +44,8 @@ def golden_c0():
 @pytest.fixture(scope="session")
 def golden_c2():
     return load_golden("scene_c2")
+
+
+@pytest.fixture(scope="session")
+def golden_backward():
+    return load_golden("backward")

@@ -18,6 +18,9 @@ and registered as `animvox._core`) and records, on seeded inputs:
                    reference's own rigging/volume/render functions: FK tables,
                    warp_voxels, resolve_collisions, build_octree,
                    rays_for_camera, render_view, forward_fit trace
+* backward.npz     backward_rays (training gradients) on the kernel scene's
+                   and the 64^3 scene's forward_fit traces, fp64 deterministic
+                   and the float32 instantiation
 * scene_c0.npz     configs[0] at full size (128^3, 256^2): SHA-256 digests of
                    every exact array plus a pixel subsample of the maps
 * scene_c2.npz     configs[2] at full size (512^3, 1024^2, C = 32 through a
@@ -345,6 +348,44 @@ def scene_fixture(sc: S.Scene, full: bool, pix_stride: int, fit_rays: int | None
     return out
 
 
+def backward_fixtures():
+    """backward_rays (_core.pyx:661-755) on two traced batches: the
+    test_backend-style kernel scene (degree 2, C = 3, normal dL/dF, dL/dA as
+    in test_backend.py:201-216) and the 64^3 posed scene's forward_fit
+    trace (degree 2, C = 16, sign-style losses as fit.py:486-488 feeds it).
+    Deterministic fp64 and the float32 instantiation."""
+    from animvox import _core
+
+    out = {}
+    k = np.load(os.path.join(HERE, "kernels.npz"))
+    rng = np.random.default_rng(31)
+    n = k["scene_origins"].shape[0]
+    dldf = rng.normal(size=(n, 3))
+    dlda = rng.normal(size=n)
+    common = (k["scene_fit_off"], k["scene_fit_idx"], k["scene_fit_t0"], k["scene_fit_t1"],
+              k["scene_dirs"], k["scene_rot_index"], k["scene_rot_inv"])
+    g64 = _core.backward_rays(*common, k["scene_flut"], dldf, dlda, 2, 3, True, 1)
+    gp = _pure.backward_rays(*common, k["scene_flut"], dldf, dlda, 2, 3)
+    assert np.array_equal(np.asarray(g64), gp)
+    g32 = _core.backward_rays(*common, np.ascontiguousarray(k["scene_flut"], dtype=np.float32),
+                              dldf.astype(np.float32), dlda.astype(np.float32), 2, 3, True, 1)
+    out.update(k_dldf=dldf, k_dlda=dlda, k_grad64=np.asarray(g64), k_grad32=np.asarray(g32))
+
+    m = np.load(os.path.join(HERE, "scene_mini.npz"))
+    sc = S.make_scene("c0", resolution=64, image=(64, 64))
+    n = int(m["fit_rays"])
+    rng = np.random.default_rng(41)
+    dldf = np.sign(rng.normal(size=(n, sc.channels))) / n
+    dlda = np.sign(rng.normal(size=n)) / n
+    common = (m["fit_off"], m["fit_idx"], m["fit_t0"], m["fit_t1"], m["rays_d"],
+              m["warp_rotation_joint"], m["rot_inv"])
+    g64 = _core.backward_rays(*common, sc.flut64(), dldf, dlda, sc.degree, sc.channels, True, 1)
+    g32 = _core.backward_rays(*common, np.ascontiguousarray(sc.flut32), dldf.astype(np.float32),
+                              dlda.astype(np.float32), sc.degree, sc.channels, True, 1)
+    out.update(m_dldf=dldf, m_dlda=dlda, m_grad64=np.asarray(g64), m_grad32=np.asarray(g32))
+    return out
+
+
 def main(which):
     t = time.time()
     if "kernels" in which:
@@ -355,6 +396,9 @@ def main(which):
         np.savez_compressed(os.path.join(HERE, "scene_mini.npz"),
                             **scene_fixture(sc, full=True, pix_stride=1, fit_rays=None))
         print("scene_mini.npz", sc.n_voxels, time.time() - t)
+    if "backward" in which:
+        np.savez_compressed(os.path.join(HERE, "backward.npz"), **backward_fixtures())
+        print("backward.npz", time.time() - t)
     if "c0" in which:
         sc = S.make_scene("c0")
         np.savez_compressed(os.path.join(HERE, "scene_c0.npz"),
@@ -368,4 +412,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["kernels", "mini", "c0", "c2"])
+    main(sys.argv[1:] or ["kernels", "mini", "backward", "c0", "c2"])

@@ -13,6 +13,7 @@ import hashlib
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 from paper_2202_05628_b200 import kinematics as KM
