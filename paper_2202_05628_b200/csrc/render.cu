@@ -48,12 +48,17 @@ namespace artemis {
 #ifndef ARTEMIS_DEDUP
 #define ARTEMIS_DEDUP 1
 #endif
+#ifndef ARTEMIS_ROW_PREFETCH
+#define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line
+#endif
 namespace {
 constexpr int kRenderWarps = 4;
 constexpr int kRenderThreads = 32 * kRenderWarps;
 constexpr int kSmemStack = ARTEMIS_SMEM_STACK;  // per-thread stack entries in shared memory
 constexpr int kStack = 100;  // <= 3 entries per two-level visit x 32 visits (64-bit keys) + slack
 constexpr int kStackBytes = kSmemStack * kRenderThreads * 4;
+// the exact cell walk keeps no DFS stack: its shared memory goes to L1
+constexpr int stack_bytes(bool dda) { return dda ? 0 : kStackBytes; }
 constexpr int kQCap = ARTEMIS_QCAP;  // leaves queued per lane per round
 constexpr int kQThresh = ARTEMIS_QTHRESH;  // warp-wide queued leaves that end a traversal phase
 constexpr int kMaxSteps = 64;        // traversal steps per phase at most
@@ -141,7 +146,11 @@ __device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2
 __device__ unsigned long long g_phase_clocks[8];
 __device__ unsigned long long g_fallbacks;
 __device__ unsigned long long g_tests;
+// shading reuse: visible entries, same-level row groups, unique rows per
+// warp round (all levels), rounds
+__device__ unsigned long long g_shade_stats[4];
 extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
+    cudaMemcpyFromSymbol(out + 13, g_shade_stats, sizeof(unsigned long long) * 4);
     cudaMemcpyFromSymbol(out, g_phase_clocks, sizeof(unsigned long long) * 7);
     cudaMemcpyFromSymbol(out + 7, g_fallbacks, sizeof(unsigned long long));
     cudaMemcpyFromSymbol(out + 8, g_tests, sizeof(unsigned long long));
@@ -152,6 +161,7 @@ extern "C" int artemis_debug_phase_clocks(unsigned long long *out, int reset) {
         cudaMemcpyToSymbol(g_fallbacks, z, sizeof(unsigned long long));
         cudaMemcpyToSymbol(g_tests, z, sizeof(unsigned long long));
         cudaMemcpyToSymbol(g_walk_stats, z, sizeof(unsigned long long) * 4);
+        cudaMemcpyToSymbol(g_shade_stats, z, sizeof(unsigned long long) * 4);
     }
     return 0;
 }
@@ -297,7 +307,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     int *s_stack = reinterpret_cast<int *>(s_raw);
     using T0 = typename std::conditional<kCamera, float, double>::type;
     constexpr int kQueueBytes = queue_bytes(kCamera);
-    unsigned char *qbase = s_raw + kStackBytes;
+    constexpr int kStackB = stack_bytes(kDDA);
+    unsigned char *qbase = s_raw + kStackB;
     uint32_t *q_id = reinterpret_cast<uint32_t *>(qbase);                            // leaf, then row
     double *q_em = reinterpret_cast<double *>(qbase + kQCap * kRenderThreads * 4);
     float4 *q_val = reinterpret_cast<float4 *>(qbase + kQCap * kRenderThreads * 12);  // a, dir
@@ -305,11 +316,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
     const int cp = kVec ? C : (C | 1);
-    float *feat = reinterpret_cast<float *>(s_raw + kStackBytes + kQueueBytes) +
+    float *feat = reinterpret_cast<float *>(s_raw + kStackB + kQueueBytes) +
                   (size_t)warp * 32 * cp;
     // per-warp work list (lane | level << 5) used to hand queued leaves to lanes
     uint16_t *wl = reinterpret_cast<uint16_t *>(
-                       s_raw + kStackBytes + kQueueBytes +
+                       s_raw + kStackB + kQueueBytes +
                        (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4)) +
                    warp * 32 * kQCap;
     if (kMode != kCount)
@@ -352,6 +363,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // exit crossing per axis, the leaf AABB exit, the cached brick
     int cc[3] = {0, 0, 0}, cs[3] = {0, 0, 0};
     double cE[3] = {0, 0, 0}, cX[3] = {0, 0, 0};
+    double ginv[3] = {0, 0, 0};  // fl(1 / dg) per axis (exact crossings, bricks.cuh)
     double t_end = 0.0;
     int cb[3] = {0, 0, 0}, cbid = -1;
     double cTb[3] = {0, 0, 0};
@@ -402,7 +414,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // while inside an occupied brick. Empty bricks cost one crossing each;
     // entering an occupied brick re-derives the other axes' cells there.
     auto brick_exit = [&](int a) {  // exact crossing of the current brick's exit plane on axis a
-        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a])
+        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a], ginv[a])
                           : CUDART_INF;
     };
     auto enter_brick = [&](unsigned advanced, double tn) {
@@ -413,9 +425,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const int cn = cs[a] > 0 ? cb[a] * 8 : cb[a] * 8 + 7;
                 cc[a] = cn;
                 cE[a] = tn;
-                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a]);
+                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a], ginv[a]);
             } else {
-                sync_axis(og[a], dg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], cE[a], cX[a]);
+                sync_axis(og[a], dg[a], ginv[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], cE[a], cX[a]);
             }
         }
     };
@@ -466,7 +478,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const int ck = (k == 0 ? cc[0] : k == 1 ? cc[1] : cc[2]) + sk;
             const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
             const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
-            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk);
+            const double ik = k == 0 ? ginv[0] : k == 1 ? ginv[1] : ginv[2];
+            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk, ik);
             const bool bchg = (ck >> 3) != (k == 0 ? cb[0] : k == 1 ? cb[1] : cb[2]);
 #pragma unroll
             for (int a = 0; a < 3; ++a)
@@ -625,7 +638,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                     cX[a] = CUDART_INF;
                 } else {
                     cs[a] = dg[a] > 0.0 ? 1 : -1;
-                    sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
+                    ginv[a] = __drcp_rn(dg[a]);
+                    sync_axis(og[a], dg[a], ginv[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
                 }
                 cb[a] = cc[a] >> 3;
             }
@@ -698,10 +712,13 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const uint4 L = __ldg(p.leaves + 2 * (size_t)q_id[qi]);
                 const uint4 L2 = __ldg(p.leaves + 2 * (size_t)q_id[qi] + 1);
                 const uint32_t fidx = L.w;
+#if ARTEMIS_ROW_PREFETCH
                 {   // the row's 9 x 128 B lines are read in phase C
                     const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
-                    for (int off = 0; off < p.coef_stride * 4; off += 128) prefetch_l2(row + off);
+                    for (int off = 0; off < (ARTEMIS_ROW_PREFETCH == 2 ? 1 : p.coef_stride * 4); off += 128)
+                        prefetch_l2(row + off);
                 }
+#endif
                 const double sigma = __longlong_as_double(((long long)L2.y << 32) | L2.x);
                 q_id[qi] = fidx | (sigma > p.sigma_dep ? kDenseFlag : 0u);
                 if constexpr (kDDA) {
@@ -769,6 +786,33 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         // Rays of a tile often hit the same leaf at the same level: lanes with
         // equal FLUT rows are grouped (__match_any_sync) and the row is read
         // once per group, then applied to every member ray.
+#ifdef ARTEMIS_PHASE_CLOCKS
+        if (kMode != kCount) {  // reuse statistics (instrumented build only)
+            unsigned vis_n = 0, uniq = 0;
+            for (int k = 0; k < kQCap; ++k) {
+                const int qme = k * kRenderThreads + tid;
+                const bool vis = nq > k && q_val[qme].x > 0.0f;
+                const uint32_t key = vis ? (q_id[qme] & ~kDenseFlag) : 0xFFFFFFFFu;
+                bool dup = false;
+                for (int k2 = 0; k2 <= k; ++k2) {
+                    const int q2 = k2 * kRenderThreads + tid;
+                    const bool v2 = nq > k2 && q_val[q2].x > 0.0f;
+                    const uint32_t key2 = v2 ? (q_id[q2] & ~kDenseFlag) : 0xFFFFFFFEu;
+                    for (int src = 0; src < 32; ++src) {
+                        const uint32_t o = __shfl_sync(0xffffffffu, key2, src);
+                        if (vis && o == key && (k2 < k || src < lane)) dup = true;
+                    }
+                }
+                vis_n += __popc(__ballot_sync(0xffffffffu, vis));
+                uniq += __popc(__ballot_sync(0xffffffffu, vis && !dup));
+            }
+            if (lane == 0) {
+                atomicAdd(&g_shade_stats[0], (unsigned long long)vis_n);
+                atomicAdd(&g_shade_stats[2], (unsigned long long)uniq);
+                atomicAdd(&g_shade_stats[3], 1ull);
+            }
+        }
+#endif
         if (kMode != kCount) {
             __syncwarp();
             uint32_t *wm = reinterpret_cast<uint32_t *>(wl + 32);  // group member masks
@@ -786,6 +830,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const bool leader = vis && lane == __ffs(grpm) - 1;
                 const unsigned ml = __ballot_sync(0xffffffffu, leader);
                 const int cnt = __popc(ml);
+#ifdef ARTEMIS_PHASE_CLOCKS
+                if (lane == 0) atomicAdd(&g_shade_stats[1], (unsigned long long)cnt);
+#endif
                 if (leader) {
                     const int slot = __popc(ml & lt);
                     wl[slot] = (uint16_t)lane;
@@ -892,7 +939,7 @@ template <int kMode, bool kCamera, bool kVec, bool kDDA>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
-    const size_t smem = kStackBytes + queue_bytes(kCamera) +
+    const size_t smem = stack_bytes(kDDA) + queue_bytes(kCamera) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4) +
                         (size_t)kRenderWarps * 32 * kQCap * 2;
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);

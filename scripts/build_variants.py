@@ -12,6 +12,12 @@ VARIANTS = {
     "q8t96": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=96", "ARTEMIS_MIN_BLOCKS=3"),
     "q4t48": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48"),
     "b3": ("ARTEMIS_MIN_BLOCKS=3",),
+    "b5": ("ARTEMIS_MIN_BLOCKS=5",),
+    "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
+    "pf1": ("ARTEMIS_ROW_PREFETCH=2",),
+    "q8": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=96"),
+    "t48": ("ARTEMIS_QTHRESH=48",),
+    "b6": ("ARTEMIS_MIN_BLOCKS=6",),
     "t96": ("ARTEMIS_QTHRESH=96",),
     "t32": ("ARTEMIS_QTHRESH=32",),
 }

@@ -16,7 +16,7 @@ fp = FramePipeline.from_scene(sc)
 L = _lib.load_library()
 fn = L.artemis_debug_phase_clocks
 fn.argtypes = [C.c_void_p, C.c_int]
-buf = (C.c_ulonglong * 13)()
+buf = (C.c_ulonglong * 17)()
 for f in range(3):
     fp.run(KM.PoseSpec.make(sc.poses[f]), sc.cameras[f][0], graph=False)
     torch.cuda.synchronize()
@@ -25,6 +25,9 @@ vals = list(buf)[:7]
 fb, tests = buf[7], buf[8]
 print(f"box tests {tests} exact fallbacks {fb} ({fb / max(tests, 1) * 100:.3f}%)")
 print(f"walk: crossings {buf[9]} cell steps {buf[10]} brick skips {buf[11]} axis syncs {buf[12]}")
+print(f"shade: visible entries {buf[13]} same-level groups {buf[14]} warp-round unique rows "
+      f"{buf[15]} rounds {buf[16]} (reuse same-level {buf[13] / max(buf[14], 1):.2f}x, "
+      f"warp-round {buf[13] / max(buf[15], 1):.2f}x)")
 tot = sum(vals)
 names = ["refill", "A traverse", "B1 exact", "B2 chain", "C shade", "retire", "tail"]
 print(" ".join(f"{n}={v / tot * 100:.1f}%" for n, v in zip(names, vals)))
