@@ -127,13 +127,6 @@ int artemis_brickmap_build(const uint64_t *codes, int64_t n, const int32_t *org,
                            const int32_t *dims, void *storage, size_t storage_bytes,
                            artemis_brickmap *out, artemis_stream stream);
 
-/* Self-test (synchronous): the cell walk computes plane crossings
- * fl((k - o) / d) as a reciprocal product plus one FMA correction instead of
- * a full division; this compares it bit for bit with the correctly rounded
- * division on n_samples seeded operands and returns the mismatch count
- * (0 expected). */
-int artemis_selftest_quotient(int64_t n_samples, uint64_t seed, int64_t *mismatches);
-
 typedef struct {
     const void *nodes;          /* artemis_pack_tree output: internal records */
     const void *leaves;         /* artemis_pack_tree output: leaf records */

@@ -140,56 +140,3 @@ extern "C" int artemis_brickmap_build(const uint64_t *codes, int64_t n, const in
                              recs, meta, meta + 1, S(stream));
 }
 
-// Self-test of the reciprocal-based quotient the cell walk uses (bricks.cuh
-// quotient) against the correctly rounded __ddiv_rn, on the operands the
-// walk sees: numerators fl(k - o) for integer planes k near o and direction
-// components spanning many binades, both signs.
-namespace {
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-    x ^= x >> 33;
-    x *= 0xff51afd7ed558ccdull;
-    x ^= x >> 33;
-    x *= 0xc4ceb9fe1a85ec53ull;
-    x ^= x >> 33;
-    return x;
-}
-__device__ __forceinline__ double unit(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
-
-__global__ void quotient_selftest_kernel(int64_t n, uint64_t seed, unsigned long long *bad) {
-    unsigned long long local = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t h0 = mix64(seed ^ (uint64_t)i * 0x9E3779B97F4A7C15ull);
-        const uint64_t h1 = mix64(h0), h2 = mix64(h1);
-        const double o = unit(h0) * 4096.0 - 1024.0;
-        const int k = (int)floor(o) + (int)(h1 % 17) - 8;
-        const double mag = exp2(unit(h1) * 40.0 - 20.0);  // 2^-20 .. 2^20
-        const double d = (h2 & 1 ? -1.0 : 1.0) * mag * (1.0 + unit(h2));
-        const double num = __dadd_rn((double)k, -o);
-        const double want = __ddiv_rn(num, d);
-        const double got = quotient(num, d, __drcp_rn(d));
-        if (__double_as_longlong(want) != __double_as_longlong(got)) ++local;
-    }
-    if (local) atomicAdd(bad, local);
-}
-}  // namespace
-
-extern "C" int artemis_selftest_quotient(int64_t n_samples, uint64_t seed, int64_t *mismatches) {
-    if (n_samples < 0 || !mismatches) return ARTEMIS_ERR_ARG;
-    unsigned long long *d = nullptr;
-    ARTEMIS_TRY(cudaMalloc(&d, sizeof(*d)));
-    ARTEMIS_TRY(cudaMemset(d, 0, sizeof(*d)));
-    quotient_selftest_kernel<<<num_sms() * 8, 256>>>(n_samples, seed, d);
-    int rc = ARTEMIS_LAUNCHED();
-    unsigned long long h = 0;
-    if (!rc) {
-        cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) {
-            set_cuda_error(e);
-            rc = ARTEMIS_ERR_CUDA;
-        }
-    }
-    cudaFree(d);
-    *mismatches = (int64_t)h;
-    return rc;
-}

@@ -59,64 +59,43 @@ __device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick 
     } while (0)
 #endif
 
-// fl(n / d) from inv = fl(1 / d) (__drcp_rn, once per ray and axis) in four
-// dependent fp64 operations instead of a full division: q0 = fl(n inv) is
-// within 1 ulp of n / d, r = n - q0 d is exact (FMA), and q0 + r inv rounded
-// once is the correctly rounded quotient (Markstein's theorem; no overflow
-// or underflow here: |n| < 2^22, |d| is a grid-space direction component).
-// ARTEMIS_EXACT_DIV=1 selects __ddiv_rn instead (tests compare the two).
-#ifndef ARTEMIS_EXACT_DIV
-#define ARTEMIS_EXACT_DIV 0
-#endif
-__device__ __forceinline__ double quotient(double n, double d, double inv) {
-#if ARTEMIS_EXACT_DIV
-    (void)inv;
-    return __ddiv_rn(n, d);
-#else
-    if (!(fabs(inv) < 1e300)) return __ddiv_rn(n, d);  // |d| subnormal: no reciprocal
-    const double q0 = __dmul_rn(n, inv);
-    const double r = __fma_rn(-q0, d, n);
-    return __fma_rn(r, inv, q0);
-#endif
-}
-
-__device__ __forceinline__ double crossing(int k, double o, double d, double inv) {
+__device__ __forceinline__ double crossing(int k, double o, double d) {
     ARTEMIS_STAT(0);
-    return quotient(__dadd_rn((double)k, -o), d, inv);
+    return __ddiv_rn(__dadd_rn((double)k, -o), d);
 }
 
 // Slab of one axis that contains distance t (entry <= t < exit), searched
 // from an estimate inside [cmin, cmax]; returns its exact entry/exit.
-__device__ __forceinline__ void sync_axis(double o, double d, double inv, double t, int cmin,
-                                          int cmax, int &c, double &E, double &X) {
+__device__ __forceinline__ void sync_axis(double o, double d, double t, int cmin, int cmax,
+                                          int &c, double &E, double &X) {
     ARTEMIS_STAT(3);
     const double est = floor(o + t * d);
     c = est < (double)cmin ? cmin : est > (double)cmax ? cmax : (int)est;
     if (d > 0.0) {  // slab c = [cross(c), cross(c+1))
-        double lo = crossing(c, o, d, inv);
+        double lo = crossing(c, o, d);
         while (c > cmin && lo > t) {
             --c;
-            lo = crossing(c, o, d, inv);
+            lo = crossing(c, o, d);
         }
-        double hi = crossing(c + 1, o, d, inv);
+        double hi = crossing(c + 1, o, d);
         while (c < cmax && hi <= t) {
             ++c;
             lo = hi;
-            hi = crossing(c + 1, o, d, inv);
+            hi = crossing(c + 1, o, d);
         }
         E = lo;
         X = hi;
     } else {  // slab c = [cross(c+1), cross(c))
-        double en = crossing(c + 1, o, d, inv);
+        double en = crossing(c + 1, o, d);
         while (c < cmax && en > t) {
             ++c;
-            en = crossing(c + 1, o, d, inv);
+            en = crossing(c + 1, o, d);
         }
-        double ex = crossing(c, o, d, inv);
+        double ex = crossing(c, o, d);
         while (c > cmin && ex <= t) {
             --c;
             en = ex;
-            ex = crossing(c, o, d, inv);
+            ex = crossing(c, o, d);
         }
         E = en;
         X = ex;

@@ -363,7 +363,6 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // exit crossing per axis, the leaf AABB exit, the cached brick
     int cc[3] = {0, 0, 0}, cs[3] = {0, 0, 0};
     double cE[3] = {0, 0, 0}, cX[3] = {0, 0, 0};
-    double ginv[3] = {0, 0, 0};  // fl(1 / dg) per axis (exact crossings, bricks.cuh)
     double t_end = 0.0;
     int cb[3] = {0, 0, 0}, cbid = -1;
     double cTb[3] = {0, 0, 0};
@@ -414,7 +413,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // while inside an occupied brick. Empty bricks cost one crossing each;
     // entering an occupied brick re-derives the other axes' cells there.
     auto brick_exit = [&](int a) {  // exact crossing of the current brick's exit plane on axis a
-        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a], ginv[a])
+        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a])
                           : CUDART_INF;
     };
     auto enter_brick = [&](unsigned advanced, double tn) {
@@ -425,9 +424,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const int cn = cs[a] > 0 ? cb[a] * 8 : cb[a] * 8 + 7;
                 cc[a] = cn;
                 cE[a] = tn;
-                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a], ginv[a]);
+                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a]);
             } else {
-                sync_axis(og[a], dg[a], ginv[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], cE[a], cX[a]);
+                sync_axis(og[a], dg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], cE[a], cX[a]);
             }
         }
     };
@@ -478,8 +477,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const int ck = (k == 0 ? cc[0] : k == 1 ? cc[1] : cc[2]) + sk;
             const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
             const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
-            const double ik = k == 0 ? ginv[0] : k == 1 ? ginv[1] : ginv[2];
-            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk, ik);
+            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk);
             const bool bchg = (ck >> 3) != (k == 0 ? cb[0] : k == 1 ? cb[1] : cb[2]);
 #pragma unroll
             for (int a = 0; a < 3; ++a)
@@ -638,8 +636,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                     cX[a] = CUDART_INF;
                 } else {
                     cs[a] = dg[a] > 0.0 ? 1 : -1;
-                    ginv[a] = __drcp_rn(dg[a]);
-                    sync_axis(og[a], dg[a], ginv[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
+                    sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
                 }
                 cb[a] = cc[a] >> 3;
             }
