@@ -280,11 +280,17 @@ int artemis_frame_destroy(artemis_frame frame);
  * canonical cells (identity warp, render.py:162-167).
  * flags: bit0 early stop, bit1 capture/replay a CUDA graph (needs a
  * non-default stream); bit2 is accepted for compatibility (the reference
- * tree arrays left/right/box_min/box_size are rebuilt every frame).
- * F (W*H, C) fp32, alpha/depth (W*H) fp32, row-major pixels. */
+ * tree arrays left/right/box_min/box_size are rebuilt every frame); bit3
+ * (ARTEMIS_FRAME_MAPS64) writes alpha/depth as double with exact fp64 entry
+ * distances, as artemis_render_rays does (the reference's FrameBuffers
+ * precision), instead of float.
+ * F (W*H, C) fp32, alpha/depth (W*H) float or double, row-major pixels. */
+#define ARTEMIS_FRAME_EARLY_STOP 1
+#define ARTEMIS_FRAME_GRAPH 2
+#define ARTEMIS_FRAME_MAPS64 8
 int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double *rot_inv,
                       int n_joints, const artemis_camera *cam, double lambda_th,
-                      double sigma_dep, int flags, float *F, float *alpha, float *depth,
+                      double sigma_dep, int flags, float *F, void *alpha, void *depth,
                       artemis_stream stream);
 
 /* Read back the last frame's counts (synchronises the stream). */
@@ -311,6 +317,29 @@ int artemis_frame_get_tree(artemis_frame frame, artemis_frame_tree *out);
  * render of the last such run (synchronises on its last event). */
 int artemis_frame_profile(artemis_frame frame, int enable);
 int artemis_frame_stage_ms(artemis_frame frame, float *ms);
+
+/* ---- Post-render frame-buffer step --------
+ * On a device-resident frame: F (n_pix, C) fp32, alpha/depth (n_pix) float
+ * (maps64 = 0) or double (maps64 = 1). Outputs fp64 (or uint8), row-major
+ * pixels; fp64 arithmetic in the reference's order (bit-equal to numpy on
+ * the same inputs).
+ * over_background: out = F + (1 - alpha) * color[c]   (render.py:98-104)
+ * composite: depth <= bg_depth ? F + (1 - alpha) * bg : bg (render.py:366-382)
+ * straight_rgba (C = 3): (clip(F / alpha, 0, 1) where alpha > 0 else 0,
+ *   alpha) as (n_pix, 4) fp64                      (assetio.py:265-275)
+ * rgba8 (C = 3): straight_rgba quantised as save_png / encode_png do,
+ *   clip(round_half_even(v * 255), 0, 255) -> (n_pix, 4) uint8
+ *                                                    (assetio.py:209-245) */
+int artemis_over_background(const float *F, const void *alpha, int maps64, int64_t n_pix,
+                            int channels, const double *color, double *out,
+                            artemis_stream stream);
+int artemis_composite(const float *F, const void *alpha, const void *depth, int maps64,
+                      int64_t n_pix, int channels, const double *bg_color,
+                      const double *bg_depth, double *out, artemis_stream stream);
+int artemis_straight_rgba(const float *F, const void *alpha, int maps64, int64_t n_pix,
+                          double *rgba, artemis_stream stream);
+int artemis_rgba8(const float *F, const void *alpha, int maps64, int64_t n_pix, uint8_t *rgba8,
+                  artemis_stream stream);
 
 /* ---- Multi-GPU tile shards ----------------------
  * With tile sharding (artemis_camera tile_start/tile_stride) each rank packs

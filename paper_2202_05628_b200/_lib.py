@@ -101,6 +101,10 @@ _SIGS = {
     "artemis_backward_workspace_bytes": (SZ, [I64, I64]),
     "artemis_backward_rays": (INT, [P, I64, P, P, P, I64, P, P, P, P, I64, INT, P, P, INT, INT,
                                     INT, INT, P, P, SZ, P]),
+    "artemis_over_background": (INT, [P, P, INT, I64, INT, P, P, P]),
+    "artemis_composite": (INT, [P, P, P, INT, I64, INT, P, P, P, P]),
+    "artemis_straight_rgba": (INT, [P, P, INT, I64, P, P]),
+    "artemis_rgba8": (INT, [P, P, INT, I64, P, P]),
     "artemis_tiles_shard_floats": (I64, [INT, INT, INT, INT, INT]),
     "artemis_tiles_pack": (INT, [P, P, P, INT, INT, INT, INT, INT, P, P]),
     "artemis_tiles_unpack": (INT, [P, INT, INT, INT, INT, INT, P, P, P, P]),

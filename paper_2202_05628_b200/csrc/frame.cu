@@ -27,8 +27,8 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
                   cudaStream_t st);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
-                  double lambda_th, double sigma_dep, int early_stop, float *F, float *A,
-                  float *D, unsigned long long *queue, cudaStream_t st);
+                  double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
+                  void *A, void *D, unsigned long long *queue, cudaStream_t st);
 
 constexpr int kMaxFrameJoints = 256;
 
@@ -102,8 +102,8 @@ int dev_alloc(T **p, size_t bytes) {
 }
 
 int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int height,
-                  int sharded, double lambda_th, double sigma_dep, int flags, float *F, float *A,
-                  float *D, cudaStream_t st) {
+                  int sharded, double lambda_th, double sigma_dep, int flags, float *F, void *A,
+                  void *D, cudaStream_t st) {
     const artemis_asset &as = f->asset;
     int rc;
     int launches = 0;
@@ -174,7 +174,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
-                       flags & 1, F, A, D,
+                       flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                        reinterpret_cast<unsigned long long *>(f->counters + 2), st);
     mark(5);
     launches += 1;
@@ -276,8 +276,8 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
 
 extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const double *rot_inv,
                                  int n_joints, const artemis_camera *cam, double lambda_th,
-                                 double sigma_dep, int flags, float *F, float *alpha,
-                                 float *depth, artemis_stream stream) {
+                                 double sigma_dep, int flags, float *F, void *alpha,
+                                 void *depth, artemis_stream stream) {
     if (!f || !cam || !F || !alpha || !depth || cam->width < 1 || cam->height < 1)
         return ARTEMIS_ERR_ARG;
     const int identity = joint_aff == nullptr;

@@ -300,13 +300,16 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
 // the ray's side of that plane has the smaller entry distance -- the order
 // the reference's `lt0 <= rt0` comparison yields (_core.pyx:345). Internal
 // tests use the fp32 filter; emitted leaves get exact fp64 intervals.
-template <int kDeg, int kMode, bool kCamera, bool kVec, bool kDDA>
+// kRays: 0 = explicit ray arrays (fp64 maps), 1 = in-kernel camera rays with
+// fp32 alpha/depth maps (frame pipeline), 2 = camera rays with fp64 maps
+template <int kDeg, int kMode, int kRays, bool kVec, bool kDDA>
 __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_kernel(RenderArgs p) {
+    constexpr bool kCamera = kRays != 0;
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
-    using T0 = typename std::conditional<kCamera, float, double>::type;
-    constexpr int kQueueBytes = queue_bytes(kCamera);
+    using T0 = typename std::conditional<kRays == 1, float, double>::type;
+    constexpr int kQueueBytes = queue_bytes(kRays == 1);
     constexpr int kStackB = stack_bytes(kDDA);
     unsigned char *qbase = s_raw + kStackB;
     uint32_t *q_id = reinterpret_cast<uint32_t *>(qbase);                            // leaf, then row
@@ -932,18 +935,18 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #endif
 }
 
-template <int kMode, bool kCamera, bool kVec, bool kDDA>
+template <int kMode, int kRays, bool kVec, bool kDDA>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
-    const size_t smem = stack_bytes(kDDA) + queue_bytes(kCamera) +
+    const size_t smem = stack_bytes(kDDA) + queue_bytes(kRays == 1) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * 4) +
                         (size_t)kRenderWarps * 32 * kQCap * 2;
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
     case D: {                                                                                   \
-        auto kern = render_kernel<D, kMode, kCamera, kVec, kDDA>;                               \
+        auto kern = render_kernel<D, kMode, kRays, kVec, kDDA>;                                 \
         if (smem > 48 * 1024)                                                                   \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         int occ = 0;                                                                            \
@@ -960,20 +963,20 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     return ARTEMIS_LAUNCHED();
 }
 
-template <int kMode, bool kCamera>
+template <int kMode, int kRays>
 int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     const bool vec = kMode != kCount && a.channels % 4 == 0 && a.coef_stride % 4 == 0 &&
                      (reinterpret_cast<uintptr_t>(a.coef) & 15) == 0;
     const bool dda = a.bm.table != nullptr;
-    if (kCamera) {  // the device pipeline always has a brick map
-        return vec ? launch_render_vec<kMode, kCamera, true, true>(degree, a, warps, st)
-                   : launch_render_vec<kMode, kCamera, false, true>(degree, a, warps, st);
+    if (kRays != 0) {  // the device pipeline always has a brick map
+        return vec ? launch_render_vec<kMode, kRays, true, true>(degree, a, warps, st)
+                   : launch_render_vec<kMode, kRays, false, true>(degree, a, warps, st);
     }
     if (dda)
-        return vec ? launch_render_vec<kMode, kCamera, true, true>(degree, a, warps, st)
-                   : launch_render_vec<kMode, kCamera, false, true>(degree, a, warps, st);
-    return vec ? launch_render_vec<kMode, kCamera, true, false>(degree, a, warps, st)
-               : launch_render_vec<kMode, kCamera, false, false>(degree, a, warps, st);
+        return vec ? launch_render_vec<kMode, kRays, true, true>(degree, a, warps, st)
+                   : launch_render_vec<kMode, kRays, false, true>(degree, a, warps, st);
+    return vec ? launch_render_vec<kMode, kRays, true, false>(degree, a, warps, st)
+               : launch_render_vec<kMode, kRays, false, false>(degree, a, warps, st);
 }
 
 static void fill_tree(RenderArgs &a, const artemis_tree_view *t) {
@@ -1011,42 +1014,56 @@ static void fill_rays(RenderArgs &a, const artemis_rays *r) {
     a.t_max = r->t_max;
 }
 
-__global__ void fill_alpha_depth(float *A, float *D, int64_t n) {
+template <typename T>
+__global__ void fill_alpha_depth(T *A, T *D, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        A[i] = 0.0f;
-        D[i] = CUDART_INF_F;
+        A[i] = T(0);
+        D[i] = T(CUDART_INF);
     }
 }
 
-// Device-pipeline render with in-kernel camera rays (frame.cu).
+// Device-pipeline render with in-kernel camera rays (frame.cu). maps64:
+// alpha/depth are double (exact fp64 maps, as the API path) instead of float.
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
-                  double lambda_th, double sigma_dep, int early_stop, float *F, float *A,
-                  float *D, unsigned long long *queue, cudaStream_t st) {
+                  double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
+                  void *A, void *D, unsigned long long *queue, cudaStream_t st) {
     RenderArgs a{};
     fill_tree(a, tree);
     fill_shade(a, shade);
     a.cam = cam_dev;
     a.queue = queue;
-    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)width * height * shade->channels * sizeof(float), st));
+    const int64_t n = (int64_t)width * height;
+    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * shade->channels * sizeof(float), st));
     if (sharded) {  // pixels of other ranks' tiles: alpha 0, depth +inf
-        const int64_t n = (int64_t)width * height;
-        fill_alpha_depth<<<(int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148), 256, 0, st>>>(A, D, n);
+        const int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148);
+        if (maps64)
+            fill_alpha_depth<double><<<g, 256, 0, st>>>(static_cast<double *>(A),
+                                                        static_cast<double *>(D), n);
+        else
+            fill_alpha_depth<float><<<g, 256, 0, st>>>(static_cast<float *>(A),
+                                                       static_cast<float *>(D), n);
     }
     a.tiles_x = (width + 7) / 8;
     a.tiles_y = (height + 3) / 4;
-    a.n_rays = (int64_t)width * height;
+    a.n_rays = n;
     a.t_min = 0.0;
     a.t_max = HUGE_VAL;
     a.stop = 1.0 - lambda_th;
     a.sigma_dep = sigma_dep;
     a.early_stop = early_stop;
     a.F = F;
-    a.A32 = A;
-    a.D32 = D;
+    if (maps64) {
+        a.A64 = static_cast<double *>(A);
+        a.D64 = static_cast<double *>(D);
+    } else {
+        a.A32 = static_cast<float *>(A);
+        a.D32 = static_cast<float *>(D);
+    }
     const int64_t warps = (int64_t)a.tiles_x * ((height + 3) / 4);
-    return launch_render_deg<kRender, true>(shade->degree, a, warps, st);
+    return maps64 ? launch_render_deg<kRender, 2>(shade->degree, a, warps, st)
+                  : launch_render_deg<kRender, 1>(shade->degree, a, warps, st);
 }
 
 __global__ void camera_rays_kernel(artemis_camera cam, double *og, double *dg, double *dw) {
@@ -1120,7 +1137,7 @@ extern "C" int artemis_render_rays(const artemis_tree_view *tree, const artemis_
     ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)rays->n_rays * shade->channels * sizeof(float),
                                 S(stream)));
     return with_queue(a, S(stream), [&] {
-        return launch_render_deg<kRender, false>(shade->degree, a,
+        return launch_render_deg<kRender, 0>(shade->degree, a,
                                                  ceil_div<int64_t>(rays->n_rays, 32), S(stream));
     });
 }
@@ -1135,7 +1152,7 @@ extern "C" int artemis_count_hits(const artemis_tree_view *tree, const artemis_r
     a.counts = counts;
     if (rays->n_rays == 0) return ARTEMIS_OK;
     return with_queue(a, S(stream), [&] {
-        return launch_render_deg<kCount, false>(0, a, ceil_div<int64_t>(rays->n_rays, 32),
+        return launch_render_deg<kCount, 0>(0, a, ceil_div<int64_t>(rays->n_rays, 32),
                                                 S(stream));
     });
 }
@@ -1164,7 +1181,7 @@ extern "C" int artemis_forward_fit(const artemis_tree_view *tree, const artemis_
     ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)rays->n_rays * shade->channels * sizeof(float),
                                 S(stream)));
     return with_queue(a, S(stream), [&] {
-        return launch_render_deg<kTrace, false>(shade->degree, a,
+        return launch_render_deg<kTrace, 0>(shade->degree, a,
                                                 ceil_div<int64_t>(rays->n_rays, 32), S(stream));
     });
 }

@@ -106,21 +106,24 @@ class FramePipeline:
         return K.camera_struct(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
                                self.lo, self.cell)
 
-    def outputs(self, width: int, height: int):
-        key = (width, height)
+    def outputs(self, width: int, height: int, maps64: bool = False):
+        key = (width, height, bool(maps64))
         if key not in self._outs:
             with torch.cuda.stream(self.stream):
                 n = width * height
-                self._outs[key] = (empty((n, self.channels), np.float32), empty(n, np.float32),
-                                   empty(n, np.float32))
+                mt = np.float64 if maps64 else np.float32
+                self._outs[key] = (empty((n, self.channels), np.float32), empty(n, mt),
+                                   empty(n, mt))
         return self._outs[key]
 
     def run(self, pose, camera, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
             early_stop: bool = True, graph: bool = True, parity: bool = False, tables=None,
-            out=None, tiles: tuple | None = None):
+            out=None, tiles: tuple | None = None, maps64: bool = False):
         """Enqueue one frame on self.stream; returns device (F, alpha, depth)
-        (fp32, row-major pixels). `pose` None renders the canonical cells.
-        `tiles` = (start, stride) renders only that tile shard (parallel.py)."""
+        (row-major pixels; F fp32, alpha/depth fp32, or fp64 with exact
+        entry distances when `maps64`). `pose` None renders the canonical
+        cells. `tiles` = (start, stride) renders only that tile shard
+        (parallel.py)."""
         L = _lib.lib()
         cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
         if tiles is not None:
@@ -133,8 +136,11 @@ class FramePipeline:
             aff = np.ascontiguousarray(t.affine34)
             rot = np.ascontiguousarray(t.rot_inv.reshape(-1, 9))
             nj = int(aff.shape[0])
-        F, A, D = out if out is not None else self.outputs(cam.width, cam.height)
-        flags = (1 if early_stop else 0) | (2 if graph else 0) | (4 if parity else 0)
+        F, A, D = out if out is not None else self.outputs(cam.width, cam.height, maps64)
+        if (A.dtype == torch.float64) != bool(maps64):
+            raise ValueError("alpha/depth buffers must be float64 exactly when maps64")
+        flags = ((1 if early_stop else 0) | (2 if graph else 0) | (4 if parity else 0)
+                 | (8 if maps64 else 0))
         check(L.artemis_frame_run(self._h, aff.ctypes.data if aff is not None else None,
                                   rot.ctypes.data if rot is not None else None, nj, C.byref(cam),
                                   float(lambda_th), float(sigma_dep), flags, ptr(F), ptr(A),

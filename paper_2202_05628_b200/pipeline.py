@@ -16,11 +16,25 @@ attributes, and return objects with the reference's field names and dtypes
 what the reference also does on the host and is not on the hot path:
 forward kinematics (J joints), argument validation, and the reshape of the
 result. Per-frame throughput work lives in frame.FramePipeline.
+
+render_frame / timed_render_frame -- the calls the reference's CLI
+(`animate`, `bench`, cli.py:295-416) and WebSocket service
+(RenderService.render_png, service.py:121-130) make once per frame -- keep
+the character resident on the device between calls: the first call for an
+asset builds a FramePipeline (canonical cells, skin weights and the FLUT
+uploaded once), later calls only upload the pose tables and camera and run
+the device frame (warp -> sort -> resolve -> build -> render) with fp64
+alpha/depth maps, exactly the API path's results. A cached pipeline is
+dropped when its asset is garbage-collected or its arrays change (data
+pointer, shape or a strided content sample).
 """
 
 from __future__ import annotations
 
+import collections
+import hashlib
 import time
+import weakref
 
 import numpy as np
 import torch
@@ -304,14 +318,141 @@ def _is_canonical(pose) -> bool:
             and not np.any(pose.global_translation))
 
 
+# ---------------------------------------------------------------------------
+# persistent device state for the per-frame entry points (CLI, service)
+
+
+def _array_sig(a) -> tuple:
+    if a is None:
+        return (None,)
+    a = np.asarray(a)
+    flat = a.reshape(-1)
+    step = max(1, flat.size // 4096)
+    h = hashlib.blake2b(np.ascontiguousarray(flat[::step]).tobytes(), digest_size=16)
+    return (a.__array_interface__["data"][0], a.shape, str(a.dtype), h.hexdigest())
+
+
+def _asset_sig(asset) -> tuple:
+    w = getattr(asset, "weights", None)
+    sk = getattr(asset, "skeleton", None)
+    return (_array_sig(asset.voxels.cells), _array_sig(asset.flut.data),
+            _array_sig(w.joint_indices if w is not None else None),
+            _array_sig(w.weights if w is not None else None), id(sk),
+            tuple(np.asarray(asset.voxels.bounds.lo, np.float64)),
+            tuple(np.asarray(asset.voxels.bounds.hi, np.float64)), int(asset.voxels.resolution))
+
+
+def _frame_eligible(asset) -> bool:
+    r = int(asset.voxels.resolution)
+    n = len(asset.voxels.cells)
+    sk = getattr(asset, "skeleton", None)
+    return (r >= 1 and r & (r - 1) == 0 and r <= (1 << MAX_GRID_BITS) and 0 < n < (1 << 30)
+            and (sk is None or len(sk.parents) <= 256) and torch.cuda.is_available())
+
+
+class _DeviceAssets:
+    """LRU of FramePipelines keyed by asset identity + content signature."""
+
+    def __init__(self, capacity: int = 2):
+        self.capacity = capacity
+        self._d: collections.OrderedDict = collections.OrderedDict()
+
+    def get(self, asset):
+        if not _frame_eligible(asset):
+            return None
+        key = id(asset)
+        sig = _asset_sig(asset)
+        ent = self._d.get(key)
+        if ent is not None:
+            ref, esig, fp = ent
+            if ref() is asset and esig == sig:
+                self._d.move_to_end(key)
+                return fp
+            self._drop(key)
+        from .frame import FramePipeline
+
+        fp = FramePipeline.from_asset(asset)
+        try:
+            ref = weakref.ref(asset, lambda _r, k=key: self._drop(k))
+        except TypeError:  # not weak-referenceable: hold it (bounded by capacity)
+            ref = (lambda a=asset: a)
+        self._d[key] = (ref, sig, fp)
+        while len(self._d) > self.capacity:
+            self._drop(next(iter(self._d)))
+        return fp
+
+    def _drop(self, key):
+        ent = self._d.pop(key, None)
+        if ent is not None:
+            ent[2].close()
+
+    def clear(self):
+        for k in list(self._d):
+            self._drop(k)
+
+
+DEVICE_ASSETS = _DeviceAssets()
+
+
+def _frame_device(asset, pose, camera, opts, timed: bool):
+    """One frame through the resident FramePipeline; (FrameBuffers, times)."""
+    fp = DEVICE_ASSETS.get(asset)
+    if fp is None:
+        return None
+    rigged = getattr(asset, "skeleton", None) is not None
+    if pose is not None and not rigged and not _is_canonical(pose):
+        raise ContractViolation("asset has no rig; only the canonical pose renders")
+    cam = KM.PinholeCamera.from_any(camera)
+    if getattr(opts, "image_size", None) is not None:
+        cam = cam.scaled(*opts.image_size)
+    use_pose = pose if (pose is not None and rigged) else None
+    fp.profile(timed)
+    F, A, D = fp.run(use_pose, cam, lambda_th=opts.lambda_th, sigma_dep=opts.sigma_dep,
+                     graph=not timed, maps64=True)
+    stage = fp.stage_ms() if timed else None
+    fp.profile(False)
+    _, n_live = fp.counts()
+    if n_live == 0:
+        warp = warp_voxels(asset.voxels, asset.weights, asset.skeleton, pose)
+        raise EmptyWarpError(warp.dropped)
+    t1 = time.perf_counter()
+    h, w = cam.height, cam.width
+    frame = T.make("FrameBuffers",
+                   features=download(F).astype(np.float64).reshape(h, w, fp.channels),
+                   alpha=download(A).reshape(h, w), depth=download(D).reshape(h, w))
+    times = None
+    if timed:
+        host = time.perf_counter() - t1
+        times = {"warp": stage["warp"] / 1e3,
+                 "build-octree": (stage["sort"] + stage["resolve"] + stage["build"]) / 1e3,
+                 "volume-render": stage["render"] / 1e3 + host}
+    return frame, times
+
+
 def render_frame(asset, pose, camera, options=None):
+    """render.py:272-281, on the asset's resident device pipeline."""
+    opts = options or T.RenderOptions()
+    out = _frame_device(asset, pose, camera, opts, timed=False)
+    if out is not None:
+        return out[0]
     octree, warp = posed_octree(asset, pose)
-    return render_view(octree, asset.flut, warp, camera, options)
+    return render_view(octree, asset.flut, warp, camera, opts)
 
 
 def timed_render_frame(asset, pose, camera, options=None):
-    """render_frame plus per-stage seconds keyed like render.py:314-318
-    (each stage synchronised so the split is real device time)."""
+    """render_frame plus per-stage seconds keyed like render.py:314-318:
+    device time of each stage (CUDA events), the host copy-out and reshape
+    counted in "volume-render"."""
+    opts = options or T.RenderOptions()
+    out = _frame_device(asset, pose, camera, opts, timed=True)
+    if out is not None:
+        return out
+    return _timed_render_frame_api(asset, pose, camera, opts)
+
+
+def _timed_render_frame_api(asset, pose, camera, options=None):
+    """Per-call device path (assets the frame pipeline does not take:
+    non-power-of-two grids); each stage synchronised for real device time."""
     opts = options or T.RenderOptions()
     rigged = getattr(asset, "skeleton", None) is not None
     sync = torch.cuda.synchronize

@@ -49,3 +49,8 @@ def golden_c2():
 @pytest.fixture(scope="session")
 def golden_backward():
     return load_golden("backward")
+
+
+@pytest.fixture(scope="session")
+def golden_post():
+    return load_golden("post")

@@ -21,6 +21,9 @@ and registered as `animvox._core`) and records, on seeded inputs:
 * backward.npz     backward_rays (training gradients) on the kernel scene's
                    and the 64^3 scene's forward_fit traces, fp64 deterministic
                    and the float32 instantiation
+* post.npz         the post-render frame-buffer step (over_background,
+                   composite, frame_to_straight_rgba, encode_png) on a seeded
+                   3-channel frame
 * scene_c0.npz     configs[0] at full size (128^3, 256^2): SHA-256 digests of
                    every exact array plus a pixel subsample of the maps
 * scene_c2.npz     configs[2] at full size (512^3, 1024^2, C = 32 through a
@@ -386,6 +389,43 @@ def backward_fixtures():
     return out
 
 
+def post_fixtures():
+    """The post-render frame-buffer step through the reference's own code
+    (render.py:98-104 over_background, :366-382 composite, assetio.py:265-275
+    frame_to_straight_rgba, :232-245 encode_png decoded back to uint8) on a
+    seeded 3-channel frame: fp32-representable premultiplied F, alpha with
+    exact zeros and values above the features (clip), depth with +inf, a
+    background depth with ties, +inf and nearer/farther pixels."""
+    import io
+
+    from PIL import Image
+
+    from animvox import assetio as AIO
+
+    rng = np.random.default_rng(77)
+    h, w = 24, 20
+    a = rng.uniform(0.0, 1.0, size=(h, w))
+    a[rng.uniform(size=(h, w)) < 0.25] = 0.0
+    a = a.astype(np.float32).astype(np.float64)
+    f = (rng.uniform(-0.1, 1.3, size=(h, w, 3)) * a[:, :, None]).astype(np.float32)
+    f = f.astype(np.float64)
+    d = rng.uniform(1.0, 3.0, size=(h, w)).astype(np.float32).astype(np.float64)
+    d[a == 0.0] = np.inf
+    bgc = rng.uniform(0.0, 1.0, size=(h, w, 3))
+    bgd = rng.uniform(1.0, 3.0, size=(h, w))
+    bgd[::5, ::3] = d[::5, ::3]  # ties go to the volume (<=)
+    bgd[1::7, :] = np.inf
+    color = np.array([0.2, 0.5, 0.9])
+    fb = R.FrameBuffers(features=f, alpha=a, depth=d)
+    over = fb.over_background(color)
+    comp = R.composite(fb, bgc, bgd)
+    rgba = AIO.frame_to_straight_rgba(f, a)
+    png = AIO.encode_png(rgba)
+    q = np.asarray(Image.open(io.BytesIO(png)).convert("RGBA"))
+    return dict(F=f, A=a, D=d, bg_color=bgc, bg_depth=bgd, color=color, over=over,
+                composite=comp, rgba=rgba, rgba8=q)
+
+
 def main(which):
     t = time.time()
     if "kernels" in which:
@@ -399,6 +439,9 @@ def main(which):
     if "backward" in which:
         np.savez_compressed(os.path.join(HERE, "backward.npz"), **backward_fixtures())
         print("backward.npz", time.time() - t)
+    if "post" in which:
+        np.savez_compressed(os.path.join(HERE, "post.npz"), **post_fixtures())
+        print("post.npz", time.time() - t)
     if "c0" in which:
         sc = S.make_scene("c0")
         np.savez_compressed(os.path.join(HERE, "scene_c0.npz"),
@@ -412,4 +455,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["kernels", "mini", "backward", "c0", "c2"])
+    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "c0", "c2"])

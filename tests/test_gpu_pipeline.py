@@ -377,3 +377,63 @@ class TestRunStream:
             for a, b in zip(g, w):
                 assert np.array_equal(a, b)
         fp.close()
+
+
+class Asset:
+    """Duck-typed CharacterAsset (render.py:106-126) over a synthetic scene."""
+
+    def __init__(self, sc, rigged=True):
+        self.voxels = Vox(sc)
+        self.flut = Flut(sc)
+        self.skeleton = sc.rig if rigged else None
+        self.weights = Weights(sc) if rigged else None
+
+
+class TestResidentFrames:
+    """render_frame / timed_render_frame on the asset's resident device
+    pipeline (CLI animate/bench, service render_png)."""
+
+    def test_matches_api_path_and_golden(self, P, mini, golden_mini):
+        from paper_2202_05628_b200.types import RenderOptions
+
+        P.DEVICE_ASSETS.clear()
+        asset = Asset(mini)
+        pose = KM.PoseSpec.make(mini.poses[0])
+        cam = mini.cameras[0][0]
+        opts = RenderOptions(lambda_th=mini.lambda_th, sigma_dep=mini.sigma_dep)
+        fb, times = P.timed_render_frame(asset, pose, cam, opts)
+        assert set(times) == {"warp", "build-octree", "volume-render"}
+        assert all(v >= 0 for v in times.values())
+        want, _ = P._timed_render_frame_api(asset, pose, cam, opts)
+        assert fb.features.dtype == np.float64 and fb.alpha.dtype == np.float64
+        assert np.array_equal(fb.features, want.features)
+        assert np.array_equal(fb.alpha, want.alpha)
+        assert np.array_equal(fb.depth, want.depth)
+        assert digest(fb.depth) == str(golden_mini["sha_depth"])
+        err = np.abs(fb.features - golden_mini["F"])
+        assert err.max() <= F_MAX and err.mean() <= F_MEAN
+        # second frame reuses the resident pipeline (graph path, no timing)
+        fp = P.DEVICE_ASSETS.get(asset)
+        fb2 = P.render_frame(asset, pose, cam, opts)
+        assert P.DEVICE_ASSETS.get(asset) is fp
+        assert np.array_equal(fb2.features, fb.features)
+        assert np.array_equal(fb2.depth, fb.depth)
+
+    def test_content_change_rebuilds_and_unrigged_canonical(self, P, mini):
+        P.DEVICE_ASSETS.clear()
+        asset = Asset(mini)
+        cam = mini.cameras[0][0]
+        pose = KM.PoseSpec.make(mini.poses[0])
+        fb = P.render_frame(asset, pose, cam)
+        fp = P.DEVICE_ASSETS.get(asset)
+        asset.flut.data = asset.flut.data.copy()
+        asset.flut.data[:, -1] *= 2.0
+        fb2 = P.render_frame(asset, pose, cam)
+        assert P.DEVICE_ASSETS.get(asset) is not fp
+        assert not np.array_equal(fb.alpha, fb2.alpha)
+        still = Asset(mini, rigged=False)
+        fb3 = P.render_frame(still, None, cam)
+        want = P._timed_render_frame_api(still, None, cam)[0]
+        assert np.array_equal(fb3.alpha, want.alpha)
+        assert np.array_equal(fb3.features, want.features)
+        P.DEVICE_ASSETS.clear()
