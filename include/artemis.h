@@ -43,7 +43,17 @@ typedef enum {
     ARTEMIS_ERR_OOM = 5,
     ARTEMIS_ERR_CUDA = 6,       /* launch failure; see artemis_last_cuda_error */
     ARTEMIS_ERR_WORKSPACE = 7,  /* workspace smaller than *_workspace_bytes */
-    ARTEMIS_ERR_NODEVICE = 8    /* no sm_100 device visible */
+    ARTEMIS_ERR_NODEVICE = 8,   /* no sm_100 device visible */
+    /* .nvo asset container (assetio.py:86-136): TruncatedAssetError, ... */
+    ARTEMIS_ASSET_TRUNCATED_HEADER = 20,
+    ARTEMIS_ASSET_BAD_MAGIC = 21,       /* MagicMismatchError */
+    ARTEMIS_ASSET_BAD_VERSION = 22,     /* AssetFormatError */
+    ARTEMIS_ASSET_ZERO_COUNT = 23,      /* CountMismatchError */
+    ARTEMIS_ASSET_TRUNCATED_LEAVES = 24,
+    ARTEMIS_ASSET_TRUNCATED_FLUT = 25,
+    ARTEMIS_ASSET_RIG_OFFSET = 26,      /* CountMismatchError */
+    ARTEMIS_ASSET_TRUNCATED_RIG = 27,
+    ARTEMIS_ASSET_TRAILING = 28         /* CountMismatchError */
 } artemis_status;
 
 const char *artemis_version(void);
@@ -317,6 +327,45 @@ int artemis_frame_get_tree(artemis_frame frame, artemis_frame_tree *out);
  * render of the last such run (synchronises on its last event). */
 int artemis_frame_profile(artemis_frame frame, int enable);
 int artemis_frame_stage_ms(artemis_frame frame, float *ms);
+
+/* ---- Device-resident asset ingestion ------
+ * The .nvo container of animvox/assetio.py:49-202 (54-byte header, leaf
+ * table of {u64 Morton code, u32 FLUT row}, f32 FLUT block, optional rig).
+ * artemis_asset_probe (host) validates the header and the leaf/FLUT extents
+ * in load_asset's order (assetio.py:88-104) and fills the info;
+ * artemis_asset_decode_leaves (device) decodes the leaf table -- copied to
+ * the device as it lies in the file -- into cells[row] (count, 3) int32
+ * (assetio.py:118-122), setting *bad_flag (device) when the rows are not a
+ * permutation (assetio.py:115-117); workspace >= 4 * count bytes. The f32
+ * FLUT block goes to artemis_flut_split_f32 unchanged.
+ * artemis_asset_decode_rig (host) decodes the rig block (assetio.py:158-202):
+ * called first with parents == NULL it validates and sizes (n_joints, k_max,
+ * name_bytes); called again with rig->k_max set and arrays of those sizes --
+ * parents (J), bind (J, 7) {qw, qx, qy, qz, tx, ty, tz}, names (name_bytes)
+ * with name_offsets (J + 1), joint_idx (count, k_max) int32 (-1 pad),
+ * weights (count, k_max) fp64 (0 pad) -- it fills them. Also checks the rig
+ * offset and trailing bytes (assetio.py:124-131). */
+typedef struct {
+    uint32_t version, resolution;
+    int64_t count;
+    int32_t degree, channels, width;
+    double lo[3], hi[3];
+    int64_t rig_offset, leaf_offset, flut_offset, flut_end;
+} artemis_asset_info;
+
+typedef struct {
+    int32_t n_joints, k_max;
+    int64_t name_bytes, end;
+} artemis_asset_rig;
+
+int artemis_asset_probe(const uint8_t *data /* host */, size_t size, artemis_asset_info *info);
+int artemis_asset_decode_leaves(const uint8_t *leaf_table, int64_t count, int32_t *cells,
+                                void *workspace, size_t workspace_bytes, int32_t *bad_flag,
+                                artemis_stream stream);
+int artemis_asset_decode_rig(const uint8_t *data /* host */, size_t size,
+                             const artemis_asset_info *info, artemis_asset_rig *rig,
+                             int32_t *parents, double *bind, char *names, int32_t *name_offsets,
+                             int32_t *joint_idx, double *weights);
 
 /* ---- Post-render frame-buffer step --------
  * On a device-resident frame: F (n_pix, C) fp32, alpha/depth (n_pix) float

@@ -25,6 +25,8 @@ DBL = C.c_double
 SZ = C.c_size_t
 
 OK, ERR_ARG, ERR_RANGE, ERR_EMPTY, ERR_DUP, ERR_OOM, ERR_CUDA, ERR_WS, ERR_NODEV = range(9)
+(ASSET_TRUNC_HEADER, ASSET_BAD_MAGIC, ASSET_BAD_VERSION, ASSET_ZERO_COUNT, ASSET_TRUNC_LEAVES,
+ ASSET_TRUNC_FLUT, ASSET_RIG_OFFSET, ASSET_TRUNC_RIG, ASSET_TRAILING) = range(20, 29)
 
 
 class BrickMap(C.Structure):
@@ -56,6 +58,17 @@ class Asset(C.Structure):
     _fields_ = [("n_voxels", I64), ("resolution", I32), ("slots", I32), ("max_joints", I32),
                 ("degree", I32), ("channels", I32), ("lo", DBL * 3), ("hi", DBL * 3),
                 ("cells", P), ("joint_idx", P), ("weights", P), ("coef", P), ("sigma", P)]
+
+
+class AssetInfo(C.Structure):
+    _fields_ = [("version", C.c_uint32), ("resolution", C.c_uint32), ("count", I64),
+                ("degree", I32), ("channels", I32), ("width", I32), ("lo", DBL * 3),
+                ("hi", DBL * 3), ("rig_offset", I64), ("leaf_offset", I64),
+                ("flut_offset", I64), ("flut_end", I64)]
+
+
+class AssetRig(C.Structure):
+    _fields_ = [("n_joints", I32), ("k_max", I32), ("name_bytes", I64), ("end", I64)]
 
 
 class FrameTree(C.Structure):
@@ -105,6 +118,10 @@ _SIGS = {
     "artemis_composite": (INT, [P, P, P, INT, I64, INT, P, P, P, P]),
     "artemis_straight_rgba": (INT, [P, P, INT, I64, P, P]),
     "artemis_rgba8": (INT, [P, P, INT, I64, P, P]),
+    "artemis_asset_probe": (INT, [P, SZ, C.POINTER(AssetInfo)]),
+    "artemis_asset_decode_leaves": (INT, [P, I64, P, P, SZ, P, P]),
+    "artemis_asset_decode_rig": (INT, [P, SZ, C.POINTER(AssetInfo), C.POINTER(AssetRig), P, P,
+                                       P, P, P, P]),
     "artemis_tiles_shard_floats": (I64, [INT, INT, INT, INT, INT]),
     "artemis_tiles_pack": (INT, [P, P, P, INT, INT, INT, INT, INT, P, P]),
     "artemis_tiles_unpack": (INT, [P, INT, INT, INT, INT, INT, P, P, P, P]),

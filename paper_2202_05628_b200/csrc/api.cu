@@ -35,6 +35,15 @@ extern "C" const char *artemis_status_string(int status) {
         case ARTEMIS_ERR_CUDA: return "CUDA error";
         case ARTEMIS_ERR_WORKSPACE: return "workspace too small";
         case ARTEMIS_ERR_NODEVICE: return "no sm_100 CUDA device";
+        case ARTEMIS_ASSET_TRUNCATED_HEADER: return "file ends inside header";
+        case ARTEMIS_ASSET_BAD_MAGIC: return "magic mismatch (expected NVO1)";
+        case ARTEMIS_ASSET_BAD_VERSION: return "unsupported container version";
+        case ARTEMIS_ASSET_ZERO_COUNT: return "declared voxel count is zero";
+        case ARTEMIS_ASSET_TRUNCATED_LEAVES: return "file ends inside leaf table";
+        case ARTEMIS_ASSET_TRUNCATED_FLUT: return "file ends inside FLUT block";
+        case ARTEMIS_ASSET_RIG_OFFSET: return "rig offset does not follow the FLUT block";
+        case ARTEMIS_ASSET_TRUNCATED_RIG: return "file ends inside rig block";
+        case ARTEMIS_ASSET_TRAILING: return "trailing bytes after the asset";
         default: return "unknown status";
     }
 }

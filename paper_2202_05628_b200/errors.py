@@ -35,6 +35,24 @@ class EmptyWarpError(ArtemisError):
         super().__init__(f"all {dropped} voxels warped out of bounds")
 
 
+class AssetFormatError(ArtemisError):
+    """Malformed .nvo container (animvox/errors.py AssetFormatError)."""
+
+    category = "asset-format"
+
+
+class TruncatedAssetError(AssetFormatError):
+    category = "asset-truncated"
+
+
+class MagicMismatchError(AssetFormatError):
+    category = "asset-magic"
+
+
+class CountMismatchError(AssetFormatError):
+    category = "asset-count"
+
+
 class DeviceError(ArtemisError):
     """The CUDA library reported a failure (status code from libartemis)."""
 

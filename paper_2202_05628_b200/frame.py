@@ -30,10 +30,12 @@ from .device import download, empty, ptr, upload
 class FramePipeline:
     def __init__(self, cells, skin_idx, skin_w, flut, degree: int, channels: int,
                  resolution: int, lo, hi, rig: KM.Rig | None = None, max_joints: int | None = None,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, device_flut=None):
+        """Host arrays are uploaded once; device tensors (cells int32 (N,3),
+        skin idx int32 / weights fp64 (N,K)) and `device_flut` = (coef fp32
+        (N, W-1), sigma fp64 (N)) are used in place (assetio.load_device)."""
         L = _lib.lib()
         self.stream = stream or torch.cuda.Stream()
-        cells = np.ascontiguousarray(cells, dtype=np.int32)
         self.n = int(cells.shape[0])
         self.degree, self.channels = int(degree), int(channels)
         self.resolution = int(resolution)
@@ -42,25 +44,34 @@ class FramePipeline:
         self.cell = (self.hi - self.lo) / self.resolution
         self.rig = rig
         self._canon = KM.canonical_globals(rig) if rig is not None else None
+
+        def dev(a, dt):
+            if isinstance(a, torch.Tensor):
+                return a.contiguous()
+            return upload(np.ascontiguousarray(a, dtype=dt), dt)
+
         with torch.cuda.stream(self.stream):
-            self.d_cells = upload(cells, np.int32)
-            self.d_jidx = upload(np.ascontiguousarray(skin_idx, dtype=np.int32), np.int32)
-            self.d_w = upload(np.ascontiguousarray(skin_w, dtype=np.float64), np.float64)
-            fl = np.asarray(flut)
-            width = fl.shape[1]
-            self.coef = empty((self.n, width - 1), np.float32)
-            self.sigma = empty(self.n, np.float64)
-            sh = self.stream.cuda_stream or None
-            if fl.dtype == np.float32:
-                d_fl = upload(fl, np.float32)
-                check(L.artemis_flut_split_f32(ptr(d_fl), self.n, width, ptr(self.coef),
-                                               ptr(self.sigma), sh), "flut_split")
+            self.d_cells = dev(cells, np.int32)
+            self.d_jidx = dev(skin_idx, np.int32)
+            self.d_w = dev(skin_w, np.float64)
+            if device_flut is not None:
+                self.coef, self.sigma = device_flut
             else:
-                d_fl = upload(fl, np.float64)
-                check(L.artemis_flut_split_f64(ptr(d_fl), self.n, width, ptr(self.coef),
-                                               ptr(self.sigma), sh), "flut_split")
-            self.stream.synchronize()
-            del d_fl
+                fl = np.asarray(flut)
+                width = fl.shape[1]
+                self.coef = empty((self.n, width - 1), np.float32)
+                self.sigma = empty(self.n, np.float64)
+                sh = self.stream.cuda_stream or None
+                if fl.dtype == np.float32:
+                    d_fl = upload(fl, np.float32)
+                    check(L.artemis_flut_split_f32(ptr(d_fl), self.n, width, ptr(self.coef),
+                                                   ptr(self.sigma), sh), "flut_split")
+                else:
+                    d_fl = upload(fl, np.float64)
+                    check(L.artemis_flut_split_f64(ptr(d_fl), self.n, width, ptr(self.coef),
+                                                   ptr(self.sigma), sh), "flut_split")
+                self.stream.synchronize()
+                del d_fl
         a = _lib.Asset()
         a.n_voxels = self.n
         a.resolution = self.resolution

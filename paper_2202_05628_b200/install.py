@@ -18,8 +18,11 @@ editing the reference, to:
 and makes the drop-ins return the reference's own result classes and raise
 its own exception classes. `uninstall()` restores the original bindings.
 
-Not covered: `kernels.backward_rays` (training gradients)
-raises NotImplementedError, so fit.py's training loop is not B200-backed.
+  assetio.load_asset / load_asset_file -> assetio.* (native rig decode,
+                                          device-resident leaves + FLUT)
+
+`kernels.backward_rays` is the B200 gradient kernel, so fit.py's training
+loop (forward_fit + backward_rays per batch) runs on the device too.
 """
 
 from __future__ import annotations
@@ -27,6 +30,7 @@ from __future__ import annotations
 import importlib
 import sys
 
+from . import assetio as _assetio
 from . import kernels as _kernels
 from . import pipeline as _pipeline
 from . import types as _types
@@ -55,6 +59,9 @@ _TARGETS = (
     ("fit", "render_view", _pipeline.render_view),
     ("cli", "timed_render_frame", _pipeline.timed_render_frame),
     ("service", "timed_render_frame", _pipeline.timed_render_frame),
+    ("assetio", "load_asset", _assetio.load_asset),
+    ("assetio", "load_asset_file", _assetio.load_asset_file),
+    ("service", "load_asset", _assetio.load_asset),
 )
 
 
@@ -93,12 +100,25 @@ def install(package: str = "animvox") -> list:
         _types.FACTORIES["CollisionResolution"] = rigging.CollisionResolution
     if render is not None:
         _types.FACTORIES["FrameBuffers"] = render.FrameBuffers
+        _types.FACTORIES["CharacterAsset"] = render.CharacterAsset
+    geometry = _module(package, "geometry")
+    if volume is not None:
+        for n in ("Bounds", "VoxelSet", "FLUT"):
+            _types.FACTORIES[n] = getattr(volume, n)
+    if rigging is not None:
+        for n in ("Skeleton", "SkinWeights"):
+            _types.FACTORIES[n] = getattr(rigging, n)
+    if geometry is not None:
+        _types.FACTORIES["RigidTransform"] = geometry.RigidTransform
     if errors is not None:
         _SAVED.setdefault((package, "_errors"), {n: getattr(_pipeline, n) for n in
                                                   ("ContractViolation", "DuplicateMortonError",
                                                    "EmptyWarpError")})
         for n in ("ContractViolation", "DuplicateMortonError", "EmptyWarpError"):
             setattr(_pipeline, n, getattr(errors, n))
+        _SAVED.setdefault((package, "_asset_errors"), dict(_assetio.ERRORS))
+        for n in _assetio.ERRORS:
+            _assetio.ERRORS[n] = getattr(errors, n)
     return done
 
 
@@ -115,6 +135,9 @@ def uninstall(package: str = "animvox") -> None:
     if fac is not None:
         _types.FACTORIES.clear()
         _types.FACTORIES.update(fac)
+    aerrs = _SAVED.pop((package, "_asset_errors"), None)
+    if aerrs is not None:
+        _assetio.ERRORS.update(aerrs)
     errs = _SAVED.pop((package, "_errors"), None)
     if errs is not None:
         for n, cls in errs.items():

@@ -381,6 +381,19 @@ class _DeviceAssets:
             self._drop(next(iter(self._d)))
         return fp
 
+    def adopt(self, asset, fp) -> None:
+        """Register an already-built pipeline for `asset` (assetio.load_asset:
+        the character was decoded straight into device memory)."""
+        key = id(asset)
+        self._drop(key)
+        try:
+            ref = weakref.ref(asset, lambda _r, k=key: self._drop(k))
+        except TypeError:
+            ref = (lambda a=asset: a)
+        self._d[key] = (ref, _asset_sig(asset), fp)
+        while len(self._d) > self.capacity:
+            self._drop(next(iter(self._d)))
+
     def _drop(self, key):
         ent = self._d.pop(key, None)
         if ent is not None:

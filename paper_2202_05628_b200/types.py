@@ -8,6 +8,10 @@ reference's own code) can consume them unchanged:
 * CollisionResolution  animvox/rigging.py:214-221
 * FrameBuffers         animvox/render.py:77-104
 * RenderOptions        animvox/render.py:34-64
+* VoxelSet, FLUT       animvox/volume.py:61-179 (what load_asset builds)
+* RigidTransform       animvox/geometry.py (rotation quaternion, translation)
+* Skeleton, SkinWeights  animvox/rigging.py:32-180
+* CharacterAsset       animvox/render.py:106-126
 
 When the reference package is installed into (install.py), the factories
 below build the reference's own classes instead, so identity checks such
@@ -122,12 +126,78 @@ class RenderOptions:
             raise ContractViolation("sigma_dep must be >= 0")
 
 
+@dataclass(frozen=True)
+class VoxelSet:
+    resolution: int
+    bounds: object
+    cells: np.ndarray
+
+    def __len__(self) -> int:
+        return self.cells.shape[0]
+
+
+@dataclass
+class FLUT:
+    data: np.ndarray
+    degree: int
+    channels: int
+
+    def __len__(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def densities(self) -> np.ndarray:
+        return self.data[:, -1]
+
+
+@dataclass(frozen=True)
+class RigidTransform:
+    rotation: np.ndarray
+    translation: np.ndarray
+
+
+@dataclass(frozen=True)
+class Skeleton:
+    names: tuple
+    parents: np.ndarray
+    bind_local: tuple
+
+
+@dataclass(frozen=True)
+class SkinWeights:
+    joint_indices: np.ndarray
+    weights: np.ndarray
+
+    @property
+    def n_voxels(self) -> int:
+        return self.joint_indices.shape[0]
+
+
+@dataclass(frozen=True)
+class CharacterAsset:
+    voxels: object
+    flut: object
+    skeleton: object = None
+    weights: object = None
+
+    @property
+    def rigged(self) -> bool:
+        return self.skeleton is not None
+
+
 # factories (rebound by install.py to the reference's classes)
 FACTORIES = {
     "VoxelOctree": VoxelOctree,
     "WarpResult": WarpResult,
     "CollisionResolution": CollisionResolution,
     "FrameBuffers": FrameBuffers,
+    "Bounds": Bounds,
+    "VoxelSet": VoxelSet,
+    "FLUT": FLUT,
+    "RigidTransform": RigidTransform,
+    "Skeleton": Skeleton,
+    "SkinWeights": SkinWeights,
+    "CharacterAsset": CharacterAsset,
 }
 
 

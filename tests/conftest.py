@@ -54,3 +54,8 @@ def golden_backward():
 @pytest.fixture(scope="session")
 def golden_post():
     return load_golden("post")
+
+
+@pytest.fixture(scope="session")
+def golden_asset():
+    return load_golden("asset")

@@ -24,6 +24,9 @@ and registered as `animvox._core`) and records, on seeded inputs:
 * post.npz         the post-render frame-buffer step (over_background,
                    composite, frame_to_straight_rgba, encode_png) on a seeded
                    3-channel frame
+* asset.npz        the .nvo container: digests of save_asset bytes and of
+                   load_asset's arrays (rigged and unrigged 64^3 character),
+                   and the exception class for each corrupted variant
 * scene_c0.npz     configs[0] at full size (128^3, 256^2): SHA-256 digests of
                    every exact array plus a pixel subsample of the maps
 * scene_c2.npz     configs[2] at full size (512^3, 1024^2, C = 32 through a
@@ -426,6 +429,59 @@ def post_fixtures():
                 composite=comp, rgba=rgba, rgba8=q)
 
 
+def asset_fixtures():
+    """The .nvo container (assetio.py:49-202) through the reference: SHA-256
+    of save_asset's bytes and of every array load_asset returns, for a rigged
+    64^3 character (C = 16) and an unrigged one; and the exception class
+    load_asset raises for each corruption of the rigged file."""
+    from animvox import assetio as AIO
+
+    out = {}
+    sc = S.make_scene("c0", resolution=64, image=(64, 64))
+    voxels, flut, skel, weights, _ = reference_objects(sc)
+    cases = {"rig": R.CharacterAsset(voxels, flut, skel, weights),
+             "still": R.CharacterAsset(voxels, flut)}
+    for name, asset in cases.items():
+        data = AIO.save_asset(asset)
+        back = AIO.load_asset(data)
+        out[f"{name}_sha_bytes"] = np.array(hashlib.sha256(data).hexdigest())
+        out[f"{name}_size"] = np.int64(len(data))
+        arrs = {"cells": back.voxels.cells, "flut": back.flut.data,
+                "lo": back.voxels.bounds.lo, "hi": back.voxels.bounds.hi}
+        if back.skeleton is not None:
+            arrs.update(parents=back.skeleton.parents,
+                        bind=np.array([[*b.rotation, *b.translation]
+                                       for b in back.skeleton.bind_local]),
+                        joint_idx=back.weights.joint_indices, weights=back.weights.weights)
+            out[f"{name}_names"] = np.array("|".join(back.skeleton.names))
+        for k, v in arrs.items():
+            out[f"{name}_sha_{k}"] = np.array(digest(v))
+        out[f"{name}_resolution"] = np.int64(back.voxels.resolution)
+    data = AIO.save_asset(cases["rig"])
+    hs = 54
+    n = len(voxels)
+    width = flut.data.shape[1]
+    flut_end = hs + 12 * n + 4 * width * n
+    bad = bytearray(data)
+    bad[hs + 8:hs + 12] = bad[hs + 20:hs + 24]  # two leaves share a FLUT row
+    corrupt = {
+        "short_header": data[:40], "magic": b"NVO2" + data[4:],
+        "version": data[:4] + (2).to_bytes(4, "little") + data[8:],
+        "zero_count": data[:12] + (0).to_bytes(8, "little") + data[20:],
+        "short_leaves": data[:hs + 12 * (n // 2)], "short_flut": data[:flut_end - 3],
+        "not_permutation": bytes(bad),
+        "rig_offset": data[:46] + (flut_end + 1).to_bytes(8, "little") + data[54:],
+        "short_rig": data[:-2], "trailing": data + b"\0",
+    }
+    for k, v in corrupt.items():
+        try:
+            AIO.load_asset(v)
+            out[f"err_{k}"] = np.array("none")
+        except Exception as exc:  # the reference's class name is the fixture
+            out[f"err_{k}"] = np.array(type(exc).__name__)
+    return out
+
+
 def main(which):
     t = time.time()
     if "kernels" in which:
@@ -442,6 +498,9 @@ def main(which):
     if "post" in which:
         np.savez_compressed(os.path.join(HERE, "post.npz"), **post_fixtures())
         print("post.npz", time.time() - t)
+    if "asset" in which:
+        np.savez_compressed(os.path.join(HERE, "asset.npz"), **asset_fixtures())
+        print("asset.npz", time.time() - t)
     if "c0" in which:
         sc = S.make_scene("c0")
         np.savez_compressed(os.path.join(HERE, "scene_c0.npz"),
@@ -455,4 +514,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "c0", "c2"])
+    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "asset", "c0", "c2"])
