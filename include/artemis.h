@@ -390,6 +390,25 @@ int artemis_straight_rgba(const float *F, const void *alpha, int maps64, int64_t
 int artemis_rgba8(const float *F, const void *alpha, int maps64, int64_t n_pix, uint8_t *rgba8,
                   artemis_stream stream);
 
+/* ---- Sparse frame read-out (end-to-end host delivery) -----------------
+ * artemis_frame_compact (device, async): the pixels of a frame with
+ * alpha > 0 or finite depth, in pixel order, as records of C + 3 32-bit
+ * words {pixel index, F[0..C), alpha, depth} (fp32), into `records`
+ * (capacity n_pix records) and the record count into *count (device int64);
+ * workspace >= artemis_compact_workspace_bytes(n_pix).
+ * artemis_host_expand (host, synchronous): rebuild the dense fp32 maps from
+ * `count` records: the `prev_count` pixels listed in prev_pixels (the
+ * buffer's previous frame) are reset to F = 0, alpha = 0, depth = +inf,
+ * then the records are written; the new pixel list goes to pixels_out.
+ * `threads` host threads. The dense maps equal the frame's own bit for bit. */
+size_t artemis_compact_workspace_bytes(int64_t n_pix);
+int artemis_frame_compact(const float *F, const void *alpha, const void *depth, int maps64,
+                          int64_t n_pix, int channels, void *records, int64_t *count,
+                          void *workspace, size_t workspace_bytes, artemis_stream stream);
+int artemis_host_expand(const void *records /* host */, int64_t count, int channels,
+                        const uint32_t *prev_pixels, int64_t prev_count, float *F, float *alpha,
+                        float *depth, uint32_t *pixels_out, int threads);
+
 /* ---- Multi-GPU tile shards ----------------------
  * With tile sharding (artemis_camera tile_start/tile_stride) each rank packs
  * the pixels of its 8x4 tiles into one contiguous shard -- tile-major, 32

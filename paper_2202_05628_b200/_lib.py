@@ -122,6 +122,9 @@ _SIGS = {
     "artemis_asset_decode_leaves": (INT, [P, I64, P, P, SZ, P, P]),
     "artemis_asset_decode_rig": (INT, [P, SZ, C.POINTER(AssetInfo), C.POINTER(AssetRig), P, P,
                                        P, P, P, P]),
+    "artemis_compact_workspace_bytes": (SZ, [I64]),
+    "artemis_frame_compact": (INT, [P, P, P, INT, I64, INT, P, P, P, SZ, P]),
+    "artemis_host_expand": (INT, [P, I64, INT, P, I64, P, P, P, P, INT]),
     "artemis_tiles_shard_floats": (I64, [INT, INT, INT, INT, INT]),
     "artemis_tiles_pack": (INT, [P, P, P, INT, INT, INT, INT, INT, P, P]),
     "artemis_tiles_unpack": (INT, [P, INT, INT, INT, INT, INT, P, P, P, P]),

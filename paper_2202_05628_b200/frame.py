@@ -16,6 +16,7 @@ kinematics over J joints (kinematics.pose_tables, rigging.py:228-247,
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -162,15 +163,106 @@ class FramePipeline:
         return F, A, D
 
     def run_stream(self, items, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
-                   early_stop: bool = True, buffers: int = 2):
+                   early_stop: bool = True, sparse: bool = True):
         """Render a sequence of (pose, camera) frames to HOST memory.
 
-        Yields (F, alpha, depth) as pinned host tensors, one triple per item,
-        in order. Frame k+1 renders while frame k's result is copied
-        device -> host on a separate copy stream (double-buffered device and
-        pinned host outputs), so the sequence runs at max(render, D2H) per
-        frame rather than their sum. A yielded triple stays valid until the
-        generator is advanced `buffers - 1` more times."""
+        Yields (F, alpha, depth) host tensors (dense fp32 maps, row-major
+        pixels), one triple per item, in order; a yielded triple stays valid
+        until the generator has been advanced twice more. Frames are
+        pipelined: frame k renders while frame k-1's result crosses PCIe on
+        the copy engine and frame k-2's is expanded on the host.
+
+        sparse=True (default) moves only the covered pixels: the device
+        compacts pixels with alpha > 0 or finite depth into records
+        (artemis_frame_compact), the copy engine moves exactly those, and
+        the host rebuilds the dense maps in place (artemis_host_expand:
+        reset the pixels the buffer's previous frame covered, write the new
+        ones) -- bit-identical maps for ~1/6 of the PCIe bytes at configs[2].
+        sparse=False copies the dense maps (4(C+2) B/pixel)."""
+        if not sparse:
+            yield from self._run_stream_dense(items, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                                              early_stop=early_stop)
+            return
+        L = _lib.lib()
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream()
+            self._stream_bufs = {}
+        cs = self._copy_stream
+        C_ = self.channels
+        R = C_ + 3
+        threads = max(1, min(16, (os.cpu_count() or 2) // 2))
+        self.last_stream_d2h_bytes = []
+
+        def bufs(w, h, b):
+            key = ("sparse", w, h, b)
+            if key not in self._stream_bufs:
+                n = w * h
+                with torch.cuda.stream(self.stream):
+                    dev = (empty((n, C_), np.float32), empty(n, np.float32), empty(n, np.float32))
+                    drec = torch.empty(n * R, dtype=torch.int32, device="cuda")
+                    dcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+                    ws = torch.empty(L.artemis_compact_workspace_bytes(n), dtype=torch.uint8,
+                                     device="cuda")
+                hrec = torch.empty(n * R, dtype=torch.int32, pin_memory=True)
+                hcnt = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+                dense = (torch.zeros((n, C_), dtype=torch.float32),
+                         torch.zeros(n, dtype=torch.float32),
+                         torch.full((n,), float("inf"), dtype=torch.float32))
+                pix = [torch.empty(n, dtype=torch.int32), 0]  # dense buffer's covered pixels
+                self._stream_bufs[key] = dict(dev=dev, drec=drec, dcnt=dcnt, ws=ws, hrec=hrec,
+                                              hcnt=hcnt, dense=dense, pix=pix,
+                                              counted=torch.cuda.Event(),
+                                              copied=torch.cuda.Event(), n=0)
+            return self._stream_bufs[key]
+
+        def launch_copy(bb):  # frame's count is on the host: move exactly its records
+            bb["counted"].synchronize()
+            n = int(bb["hcnt"][0])
+            bb["n"] = n
+            cs.wait_event(bb["counted"])
+            if n:
+                with torch.cuda.stream(cs):
+                    bb["hrec"][:n * R].copy_(bb["drec"][:n * R], non_blocking=True)
+            bb["copied"].record(cs)
+            self.last_stream_d2h_bytes.append(n * R * 4 + 8)
+
+        def expand(bb):
+            bb["copied"].synchronize()
+            F, A, D = bb["dense"]
+            pix = bb["pix"]
+            n = bb["n"]
+            check(L.artemis_host_expand(bb["hrec"].data_ptr() if n else None, n, C_,
+                                        pix[0].data_ptr() if pix[1] else None, pix[1],
+                                        F.data_ptr(), A.data_ptr(), D.data_ptr(),
+                                        pix[0].data_ptr(), threads), "host_expand")
+            pix[1] = n
+            return bb["dense"]
+
+        pending = []
+        for k, (pose, camera) in enumerate(items):
+            cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
+            bb = bufs(cam.width, cam.height, k % 2)
+            self.stream.wait_event(bb["copied"])  # its records buffer has been read out
+            F, A, D = self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                               early_stop=early_stop, out=bb["dev"])
+            n_pix = cam.width * cam.height
+            check(L.artemis_frame_compact(ptr(F), ptr(A), ptr(D), 0, n_pix, C_, ptr(bb["drec"]),
+                                          ptr(bb["dcnt"]), ptr(bb["ws"]), bb["ws"].numel(),
+                                          self.stream.cuda_stream or None), "frame_compact")
+            with torch.cuda.stream(self.stream):
+                bb["hcnt"].copy_(bb["dcnt"], non_blocking=True)
+            bb["counted"].record(self.stream)
+            pending.append(bb)
+            if len(pending) >= 2:
+                launch_copy(pending[-2])
+            if len(pending) >= 3:
+                yield expand(pending.pop(0))
+        if pending:  # the last frame's copy is not launched yet
+            launch_copy(pending[-1])
+        for bb in pending:
+            yield expand(bb)
+
+    def _run_stream_dense(self, items, *, lambda_th, sigma_dep, early_stop, buffers: int = 2):
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream()
             self._stream_bufs = {}
@@ -180,8 +272,6 @@ class FramePipeline:
             cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
             n = cam.width * cam.height
             b = k % buffers
-            # device + pinned host buffers persist across calls (allocation
-            # and graph capture happen once per image size)
             key = (cam.width, cam.height, b)
             if key not in self._stream_bufs:
                 with torch.cuda.stream(self.stream):
