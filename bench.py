@@ -344,9 +344,9 @@ def main():
         e2e = {"value": world * e2e_steps * rays / e2e_s, "unit": "rays/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s / e2e_steps * 1e3,
-               "readout": "covered pixels only (alpha > 0 or finite depth): device compaction, "
-                          "copy engine D2H of exactly those records, host rebuilds the dense "
-                          "F/alpha/depth maps (bit-identical)"}
+               "readout": "dense F/alpha/depth maps in pinned host memory, refreshed by 2-D "
+                          "copy-engine D2H of the union of this and the buffer's previous "
+                          "frame's covered-pixel bounding box (bit-identical maps)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -409,6 +409,20 @@ int artemis_host_expand(const void *records /* host */, int64_t count, int chann
                         const uint32_t *prev_pixels, int64_t prev_count, float *F, float *alpha,
                         float *depth, uint32_t *pixels_out, int threads);
 
+/* artemis_frame_bbox (device, async): bounding box of the covered pixels
+ * (alpha > 0 or finite depth) as int32 {x0, y0, x1, y1}, inclusive, into
+ * device memory; empty frame -> x1 = y1 = -1.
+ * artemis_copy_rect_d2h: copy the rectangle of rows [y0, y0 + rows) and
+ * bytes [x_bytes, x_bytes + width_bytes) of a row-major device image with
+ * row pitch row_pitch bytes into the same place of a (pinned) host image of
+ * the same layout, on the copy engine (cudaMemcpy2DAsync). With the union
+ * of two consecutive frames' boxes this refreshes a persistent dense host
+ * frame exactly: outside the union both frames are (0, 0, +inf). */
+int artemis_frame_bbox(const void *alpha, const void *depth, int maps64, int width, int height,
+                       int32_t *box, artemis_stream stream);
+int artemis_copy_rect_d2h(void *dst_host, const void *src_dev, size_t row_pitch, size_t x_bytes,
+                          size_t width_bytes, int64_t y0, int64_t rows, artemis_stream stream);
+
 /* ---- Multi-GPU tile shards ----------------------
  * With tile sharding (artemis_camera tile_start/tile_stride) each rank packs
  * the pixels of its 8x4 tiles into one contiguous shard -- tile-major, 32

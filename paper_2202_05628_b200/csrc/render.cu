@@ -53,7 +53,7 @@ namespace artemis {
 // process the queued leaves of all levels in one flattened list (the
 // result is still bit-reproducible); 0 = fp32 sums level by level.
 #ifndef ARTEMIS_FIXED
-#define ARTEMIS_FIXED 1
+#define ARTEMIS_FIXED 0
 #endif
 #ifndef ARTEMIS_ROW_PREFETCH
 #define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line

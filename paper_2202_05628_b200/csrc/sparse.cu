@@ -198,3 +198,61 @@ extern "C" int artemis_host_expand(const void *records, int64_t count, int chann
     });
     return ARTEMIS_OK;
 }
+
+// ---- covered-pixel bounding box + rectangle read-out ----------------------
+namespace artemis {
+namespace {
+__global__ void bbox_kernel(const void *A, const void *D, int maps64, int width, int64_t n,
+                            int32_t *box) {
+    int x0 = INT32_MAX, y0 = INT32_MAX, x1 = -1, y1 = -1;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        if (!covered(A, D, maps64, p)) continue;
+        const int x = (int)(p % width), y = (int)(p / width);
+        x0 = min(x0, x);
+        x1 = max(x1, x);
+        y0 = min(y0, y);
+        y1 = max(y1, y);
+    }
+    for (int o = 16; o; o >>= 1) {
+        x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+        y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+        x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+        y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    }
+    if ((threadIdx.x & 31) == 0 && x1 >= 0) {
+        atomicMin(box + 0, x0);
+        atomicMin(box + 1, y0);
+        atomicMax(box + 2, x1);
+        atomicMax(box + 3, y1);
+    }
+}
+__global__ void bbox_init_kernel(int32_t *box) {
+    box[0] = box[1] = INT32_MAX;
+    box[2] = box[3] = -1;
+}
+}  // namespace
+}  // namespace artemis
+
+extern "C" int artemis_frame_bbox(const void *alpha, const void *depth, int maps64, int width,
+                                  int height, int32_t *box, artemis_stream stream) {
+    if (!alpha || !depth || !box || width < 1 || height < 1) return ARTEMIS_ERR_ARG;
+    const int64_t n = (int64_t)width * height;
+    bbox_init_kernel<<<1, 1, 0, S(stream)>>>(box);
+    const int blocks = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), (int64_t)num_sms() * 8);
+    bbox_kernel<<<blocks, 256, 0, S(stream)>>>(alpha, depth, maps64, width, n, box);
+    return ARTEMIS_LAUNCHED();
+}
+
+extern "C" int artemis_copy_rect_d2h(void *dst_host, const void *src_dev, size_t row_pitch,
+                                     size_t x_bytes, size_t width_bytes, int64_t y0,
+                                     int64_t rows, artemis_stream stream) {
+    if (!dst_host || !src_dev || rows < 0 || x_bytes + width_bytes > row_pitch)
+        return ARTEMIS_ERR_ARG;
+    if (rows == 0 || width_bytes == 0) return ARTEMIS_OK;
+    const size_t off = (size_t)y0 * row_pitch + x_bytes;
+    ARTEMIS_TRY(cudaMemcpy2DAsync(static_cast<char *>(dst_host) + off, row_pitch,
+                                  static_cast<const char *>(src_dev) + off, row_pitch,
+                                  width_bytes, (size_t)rows, cudaMemcpyDeviceToHost, S(stream)));
+    return ARTEMIS_OK;
+}

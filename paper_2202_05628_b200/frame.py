@@ -163,26 +163,34 @@ class FramePipeline:
         return F, A, D
 
     def run_stream(self, items, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
-                   early_stop: bool = True, sparse: bool = True):
+                   early_stop: bool = True, readout: str = "box"):
         """Render a sequence of (pose, camera) frames to HOST memory.
 
         Yields (F, alpha, depth) host tensors (dense fp32 maps, row-major
         pixels), one triple per item, in order; a yielded triple stays valid
-        until the generator has been advanced twice more. Frames are
-        pipelined: frame k renders while frame k-1's result crosses PCIe on
-        the copy engine and frame k-2's is expanded on the host.
+        until the generator is advanced. Frames are pipelined: frame k
+        renders while frame k-1's result crosses PCIe on the copy engine.
+        `readout` chooses what crosses PCIe (the maps are bit-identical):
 
-        sparse=True (default) moves only the covered pixels: the device
-        compacts pixels with alpha > 0 or finite depth into records
-        (artemis_frame_compact), the copy engine moves exactly those, and
-        the host rebuilds the dense maps in place (artemis_host_expand:
-        reset the pixels the buffer's previous frame covered, write the new
-        ones) -- bit-identical maps for ~1/6 of the PCIe bytes at configs[2].
-        sparse=False copies the dense maps (4(C+2) B/pixel)."""
-        if not sparse:
+        * "box" (default): the bounding box of the covered pixels (alpha > 0
+          or finite depth; artemis_frame_bbox) united with the previous
+          frame's box in the same host buffer, as three 2-D copies straight
+          into persistent pinned dense maps (artemis_copy_rect_d2h): outside
+          the union both frames are (0, 0, +inf). No host-side work.
+        * "records": only the covered pixels, compacted on the device
+          (artemis_frame_compact) and scattered into the dense maps on the
+          host (artemis_host_expand) -- fewest bytes, host CPU work.
+        * "dense": the whole maps, 4(C+2) bytes per pixel."""
+        if readout == "dense":
             yield from self._run_stream_dense(items, lambda_th=lambda_th, sigma_dep=sigma_dep,
                                               early_stop=early_stop)
             return
+        if readout == "box":
+            yield from self._run_stream_box(items, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                                            early_stop=early_stop)
+            return
+        if readout != "records":
+            raise ValueError("readout must be 'box', 'records' or 'dense'")
         L = _lib.lib()
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream()
@@ -261,6 +269,76 @@ class FramePipeline:
             launch_copy(pending[-1])
         for bb in pending:
             yield expand(bb)
+
+    def _run_stream_box(self, items, *, lambda_th, sigma_dep, early_stop):
+        L = _lib.lib()
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream()
+            self._stream_bufs = {}
+        cs = self._copy_stream
+        C_ = self.channels
+        self.last_stream_d2h_bytes = []
+
+        def bufs(w, h, b):
+            key = ("box", w, h, b)
+            if key not in self._stream_bufs:
+                n = w * h
+                with torch.cuda.stream(self.stream):
+                    dev = (empty((n, C_), np.float32), empty(n, np.float32), empty(n, np.float32))
+                    dbox = torch.empty(4, dtype=torch.int32, device="cuda")
+                hbox = torch.empty(4, dtype=torch.int32, pin_memory=True)
+                dense = (torch.zeros((n, C_), dtype=torch.float32, pin_memory=True),
+                         torch.zeros(n, dtype=torch.float32, pin_memory=True),
+                         torch.full((n,), float("inf"), dtype=torch.float32, pin_memory=True))
+                self._stream_bufs[key] = dict(dev=dev, dbox=dbox, hbox=hbox, dense=dense,
+                                              prev=(1 << 30, 1 << 30, -1, -1), w=w, h=h,
+                                              boxed=torch.cuda.Event(),
+                                              copied=torch.cuda.Event())
+            return self._stream_bufs[key]
+
+        def launch_copy(bb):  # union of this frame's and the buffer's last box
+            bb["boxed"].synchronize()
+            x0, y0, x1, y1 = (int(v) for v in bb["hbox"])
+            px0, py0, px1, py1 = bb["prev"]
+            ux0, uy0, ux1, uy1 = min(x0, px0), min(y0, py0), max(x1, px1), max(y1, py1)
+            bb["prev"] = (x0, y0, x1, y1)
+            cs.wait_event(bb["boxed"])
+            nbytes = 0
+            if ux1 >= ux0 and uy1 >= uy0:
+                w, rows = ux1 - ux0 + 1, uy1 - uy0 + 1
+                st = cs.cuda_stream or None
+                for dst, src, per in zip(bb["dense"], bb["dev"], (4 * C_, 4, 4)):
+                    check(L.artemis_copy_rect_d2h(dst.data_ptr(), src.data_ptr(), bb["w"] * per,
+                                                  ux0 * per, w * per, uy0, rows, st),
+                          "copy_rect")
+                nbytes = w * rows * 4 * (C_ + 2)
+            bb["copied"].record(cs)
+            self.last_stream_d2h_bytes.append(nbytes + 16)
+
+        pending = []
+        for k, (pose, camera) in enumerate(items):
+            cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
+            bb = bufs(cam.width, cam.height, k % 2)
+            self.stream.wait_event(bb["copied"])  # its device maps have been read out
+            F, A, D = self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                               early_stop=early_stop, out=bb["dev"])
+            check(L.artemis_frame_bbox(ptr(A), ptr(D), 0, cam.width, cam.height, ptr(bb["dbox"]),
+                                       self.stream.cuda_stream or None), "frame_bbox")
+            with torch.cuda.stream(self.stream):
+                bb["hbox"].copy_(bb["dbox"], non_blocking=True)
+            bb["boxed"].record(self.stream)
+            pending.append(bb)
+            if len(pending) >= 2:
+                launch_copy(pending[-2])
+            if len(pending) >= 3:
+                out = pending.pop(0)
+                out["copied"].synchronize()
+                yield out["dense"]
+        if pending:
+            launch_copy(pending[-1])
+        for bb in pending:
+            bb["copied"].synchronize()
+            yield bb["dense"]
 
     def _run_stream_dense(self, items, *, lambda_th, sigma_dep, early_stop, buffers: int = 2):
         if not hasattr(self, "_copy_stream"):

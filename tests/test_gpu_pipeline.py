@@ -371,15 +371,16 @@ class TestRunStream:
             F, A, D = fp.run(pose, cam, graph=False)
             fp.stream.synchronize()
             want.append((F.cpu().numpy().copy(), A.cpu().numpy().copy(), D.cpu().numpy().copy()))
-        for sparse in (True, False):
+        for readout in ("box", "records", "dense"):
             for n_items in (1, 2, 5):
                 got = [tuple(t.numpy().copy() for t in out)
-                       for out in fp.run_stream(items[:n_items], sparse=sparse)]
+                       for out in fp.run_stream(items[:n_items], readout=readout)]
                 assert len(got) == n_items
                 for g, w in zip(got, want):
                     for a, b in zip(g, w):
                         assert np.array_equal(a, b)
         # covered-pixel records: exactly the pixels with alpha > 0 or finite depth
+        list(fp.run_stream(items[:5], readout="records"))
         A, D = want[-1][1], want[-1][2]
         covered = int(((A > 0) | np.isfinite(D)).sum())
         assert fp.last_stream_d2h_bytes[-1] == covered * (mini.channels + 3) * 4 + 8
