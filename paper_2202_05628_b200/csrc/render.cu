@@ -37,7 +37,7 @@ namespace artemis {
 #define ARTEMIS_SMEM_STACK 28
 #endif
 #ifndef ARTEMIS_QCAP
-#define ARTEMIS_QCAP (ARTEMIS_FIXED ? 5 : 6)
+#define ARTEMIS_QCAP 6
 #endif
 #ifndef ARTEMIS_QTHRESH
 #define ARTEMIS_QTHRESH 64
@@ -47,13 +47,6 @@ namespace artemis {
 #endif
 #ifndef ARTEMIS_DEDUP
 #define ARTEMIS_DEDUP 1
-#endif
-// Feature accumulation: 1 = 64-bit fixed point (2^-32 units) with shared
-// memory integer atomics -- exact, order-independent sums, so shading can
-// process the queued leaves of all levels in one flattened list (the
-// result is still bit-reproducible); 0 = fp32 sums level by level.
-#ifndef ARTEMIS_FIXED
-#define ARTEMIS_FIXED 0
 #endif
 #ifndef ARTEMIS_ROW_PREFETCH
 #define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line
@@ -326,9 +319,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
     const int cp = kVec ? C : (C | 1);
-    // per-ray feature sums: fp32, or 64-bit fixed point (ARTEMIS_FIXED)
-    constexpr bool kFix = ARTEMIS_FIXED && kMode != kCount;
-    using FeatT = typename std::conditional<kFix, unsigned long long, float>::type;
+    using FeatT = float;  // per-ray feature sums
     FeatT *feat = reinterpret_cast<FeatT *>(s_raw + kStackB + kQueueBytes) +
                   (size_t)warp * 32 * cp;
     // per-warp work list (lane | level << 5) used to hand queued leaves to
@@ -833,91 +824,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #ifndef ARTEMIS_NOSHADE
 #define ARTEMIS_NOSHADE 0
 #endif
-        if (kFix && !ARTEMIS_NOSHADE) {
-            // all levels at once: same-level row groups (__match_any_sync) are
-            // listed level after level, then handed to lane groups in passes;
-            // a ray may be a member of several items of one pass, which the
-            // order-independent fixed-point sums make harmless
-            __syncwarp();
-            int n_items = 0;
-            for (int k = 0; k < kQCap; ++k) {
-                if (!__any_sync(0xffffffffu, nq > k)) break;
-                const int qme = k * kRenderThreads + tid;
-                const bool vis = nq > k && q_val[qme].x > 0.0f;
-                const uint32_t key = vis ? (q_id[qme] & ~kDenseFlag) : (0x80000000u | (uint32_t)lane);
-                const unsigned grpm = __match_any_sync(0xffffffffu, key);
-                const bool leader = vis && lane == __ffs(grpm) - 1;
-                const unsigned ml = __ballot_sync(0xffffffffu, leader);
-                if (leader) {
-                    const int slot = n_items + __popc(ml & lt);
-                    wl[slot] = (uint16_t)(lane | (k << 5));
-                    wm[slot] = grpm;
-                }
-                n_items += __popc(ml);
-            }
-            __syncwarp();
-            constexpr float kToFixF = 4294967296.0f;  // 2^32 (exact scaling)
-            for (int item = grp; item - grp < n_items; item += hpi) {
-                if (item >= n_items) continue;
-                const int e = (int)wl[item];
-                const int s0 = e & 31, k = e >> 5;
-                unsigned members = wm[item];
-                const uint32_t bf = q_id[k * kRenderThreads + wbase + s0] & ~kDenseFlag;
-                if (kVec) {
-                    const float4 *row = reinterpret_cast<const float4 *>(
-                        p.coef + (size_t)bf * p.coef_stride);
-                    for (int c4 = q; c4 < units; c4 += lph) {
-                        float4 v[H];
-#pragma unroll
-                        for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
-                        unsigned mm = members;
-                        while (mm) {
-                            const int s = __ffs(mm) - 1;
-                            mm &= mm - 1;
-                            const float4 bv = q_val[k * kRenderThreads + wbase + s];
-                            float Y[H];
-                            sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
-                            float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
-#pragma unroll
-                            for (int h = 0; h < H; ++h) {
-                                ax = fmaf(v[h].x, Y[h], ax);
-                                ay = fmaf(v[h].y, Y[h], ay);
-                                az = fmaf(v[h].z, Y[h], az);
-                                aw = fmaf(v[h].w, Y[h], aw);
-                            }
-                            FeatT *dst = feat + s * cp + 4 * c4;
-                            atomicAdd(reinterpret_cast<unsigned long long *>(dst) + 0,
-                                      (unsigned long long)__float2ll_rn(bv.x * ax * kToFixF));
-                            atomicAdd(reinterpret_cast<unsigned long long *>(dst) + 1,
-                                      (unsigned long long)__float2ll_rn(bv.x * ay * kToFixF));
-                            atomicAdd(reinterpret_cast<unsigned long long *>(dst) + 2,
-                                      (unsigned long long)__float2ll_rn(bv.x * az * kToFixF));
-                            atomicAdd(reinterpret_cast<unsigned long long *>(dst) + 3,
-                                      (unsigned long long)__float2ll_rn(bv.x * aw * kToFixF));
-                        }
-                    }
-                } else {
-                    const float *row = p.coef + (size_t)bf * p.coef_stride;
-                    while (members) {
-                        const int s = __ffs(members) - 1;
-                        members &= members - 1;
-                        const float4 bv = q_val[k * kRenderThreads + wbase + s];
-                        float Y[H];
-                        sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
-                        for (int c = q; c < C; c += lph) {
-                            float acc_c = 0.0f;
-#pragma unroll
-                            for (int h = 0; h < H; ++h)
-                                acc_c = fmaf(__ldg(row + h * C + c), Y[h], acc_c);
-                            atomicAdd(reinterpret_cast<unsigned long long *>(feat + s * cp + c),
-                                      (unsigned long long)__float2ll_rn(bv.x * acc_c * kToFixF));
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        if (!kFix && kMode != kCount && !ARTEMIS_NOSHADE) {
+        if (kMode != kCount && !ARTEMIS_NOSHADE) {
             __syncwarp();
             for (int k = 0; k < kQCap; ++k) {
                 if (!__any_sync(0xffffffffu, nq > k)) break;
@@ -1024,11 +931,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 fm &= fm - 1;
                 const int64_t r = __shfl_sync(0xffffffffu, ray, s);
                 for (int c = lane; c < C; c += 32) {
-                    if constexpr (kFix)
-                        p.F[r * C + c] = (float)((double)(long long)feat[s * cp + c] *
-                                                 2.3283064365386963e-10);  // 2^-32
-                    else
-                        p.F[r * C + c] = feat[s * cp + c];
+                    p.F[r * C + c] = feat[s * cp + c];
                     feat[s * cp + c] = FeatT(0);
                 }
             }
@@ -1047,7 +950,7 @@ template <int kMode, int kRays, bool kVec, bool kDDA>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
-    const size_t feat_bytes = (ARTEMIS_FIXED && kMode != kCount) ? 8 : 4;
+    const size_t feat_bytes = 4;
     const size_t smem = stack_bytes(kDDA) + queue_bytes(kRays == 1) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * feat_bytes) +
                         (size_t)kRenderWarps * 32 * kQCap * (2 + 4);

@@ -15,10 +15,6 @@ VARIANTS = {
     "b5": ("ARTEMIS_MIN_BLOCKS=5",),
     "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
     "noshade": ("ARTEMIS_NOSHADE=1",),
-    "fixed0": ("ARTEMIS_FIXED=0",),
-    "fixed_q6": ("ARTEMIS_QCAP=6", "ARTEMIS_MIN_BLOCKS=3"),
-    "fixed_t48": ("ARTEMIS_QTHRESH=48",),
-    "fixed_t80": ("ARTEMIS_QTHRESH=80",),
     "noshade_nopf": ("ARTEMIS_NOSHADE=1", "ARTEMIS_ROW_PREFETCH=0"),
     "pf1": ("ARTEMIS_ROW_PREFETCH=2",),
     "q8": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=96"),
