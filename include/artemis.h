@@ -293,11 +293,15 @@ int artemis_frame_destroy(artemis_frame frame);
  * tree arrays left/right/box_min/box_size are rebuilt every frame); bit3
  * (ARTEMIS_FRAME_MAPS64) writes alpha/depth as double with exact fp64 entry
  * distances, as artemis_render_rays does (the reference's FrameBuffers
- * precision), instead of float.
+ * precision), instead of float; bit4 (ARTEMIS_FRAME_REUSE_TREE) renders
+ * another view of the tree the previous run built (multi-view / stereo:
+ * one warp + rebuild per pose), skipping warp, sort, resolve and build --
+ * the pose tables passed must be the ones that tree was built with.
  * F (W*H, C) fp32, alpha/depth (W*H) float or double, row-major pixels. */
 #define ARTEMIS_FRAME_EARLY_STOP 1
 #define ARTEMIS_FRAME_GRAPH 2
 #define ARTEMIS_FRAME_MAPS64 8
+#define ARTEMIS_FRAME_REUSE_TREE 16
 int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double *rot_inv,
                       int n_joints, const artemis_camera *cam, double lambda_th,
                       double sigma_dep, int flags, float *F, void *alpha, void *depth,

@@ -112,6 +112,20 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         if (prof) cudaEventRecord(f->ev[k], st);
     };
     mark(0);
+    if (flags & 16) {  // ARTEMIS_FRAME_REUSE_TREE: another view of the last posed tree
+        ARTEMIS_TRY(cudaMemsetAsync(f->counters + 2, 0, 2 * sizeof(int32_t), st));
+        for (int k = 1; k <= 4; ++k) mark(k);
+        artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution,
+                             &f->bmap};
+        artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
+                           as.channels, 0};
+        rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th,
+                           sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
+                           reinterpret_cast<unsigned long long *>(f->counters + 2), st);
+        mark(5);
+        f->launches = 1;
+        return rc;
+    }
     // counters: [0] in-bounds, [1] live leaves, [2..3] render ray queue (u64)
     ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 4 * sizeof(int32_t), st));
     rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,

@@ -130,12 +130,14 @@ class FramePipeline:
 
     def run(self, pose, camera, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
             early_stop: bool = True, graph: bool = True, parity: bool = False, tables=None,
-            out=None, tiles: tuple | None = None, maps64: bool = False):
+            out=None, tiles: tuple | None = None, maps64: bool = False,
+            reuse_tree: bool = False):
         """Enqueue one frame on self.stream; returns device (F, alpha, depth)
         (row-major pixels; F fp32, alpha/depth fp32, or fp64 with exact
         entry distances when `maps64`). `pose` None renders the canonical
         cells. `tiles` = (start, stride) renders only that tile shard
-        (parallel.py)."""
+        (parallel.py). `reuse_tree` renders another view of the tree the
+        previous run built for the same pose (multi-view, stereo eyes)."""
         L = _lib.lib()
         cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
         if tiles is not None:
@@ -152,7 +154,7 @@ class FramePipeline:
         if (A.dtype == torch.float64) != bool(maps64):
             raise ValueError("alpha/depth buffers must be float64 exactly when maps64")
         flags = ((1 if early_stop else 0) | (2 if graph else 0) | (4 if parity else 0)
-                 | (8 if maps64 else 0))
+                 | (8 if maps64 else 0) | (16 if reuse_tree else 0))
         check(L.artemis_frame_run(self._h, aff.ctypes.data if aff is not None else None,
                                   rot.ctypes.data if rot is not None else None, nj, C.byref(cam),
                                   float(lambda_th), float(sigma_dep), flags, ptr(F), ptr(A),
@@ -161,6 +163,22 @@ class FramePipeline:
         if cur != self.stream:
             cur.wait_stream(self.stream)  # consumers on the caller's stream see the frame
         return F, A, D
+
+    def render_views(self, pose, cameras, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
+                     early_stop: bool = True, graph: bool = True, tables=None):
+        """One pose, several cameras (configs[1] views, configs[4] stereo
+        eyes): warp + rebuild once, then one render per camera. Returns a
+        list of device (F, alpha, depth) clones, one per camera."""
+        t = tables if tables is not None or pose is None or self.rig is None \
+            else self.tables(pose)
+        outs = []
+        for i, cam in enumerate(cameras):
+            F, A, D = self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                               early_stop=early_stop, graph=graph, tables=t,
+                               reuse_tree=i > 0)
+            with torch.cuda.stream(self.stream):
+                outs.append((F.clone(), A.clone(), D.clone()))
+        return outs
 
     def run_stream(self, items, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
                    early_stop: bool = True, readout: str = "box"):
