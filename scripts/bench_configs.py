@@ -31,6 +31,7 @@ for name in names:
     t0 = time.time()
     frames = 64 if name == "c3" else max(steps + 3, 4)
     sc = S.make_scene(name, frames=frames)
+    frames = len(sc.poses)
     fp = FramePipeline.from_scene(sc)
     gen_s = time.time() - t0
     st = fp.stream
@@ -45,7 +46,7 @@ for name in names:
                    reuse_tree=v > 0)
 
     for f in range(3):
-        step(f)
+        step(f % frames)
     st.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(n_steps)]
