@@ -15,6 +15,9 @@ VARIANTS = {
     "b5": ("ARTEMIS_MIN_BLOCKS=5",),
     "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
     "noshade": ("ARTEMIS_NOSHADE=1",),
+    "q5t56": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=56"),
+    "q5t64": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=64"),
+    "q4t48b": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48"),
     "noshade_nopf": ("ARTEMIS_NOSHADE=1", "ARTEMIS_ROW_PREFETCH=0"),
     "pf1": ("ARTEMIS_ROW_PREFETCH=2",),
     "q8": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=96"),
