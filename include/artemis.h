@@ -222,6 +222,30 @@ int artemis_backward_rays(const int64_t *offsets, int64_t n_rays, const int64_t 
                           int deterministic, void *grad, void *workspace,
                           size_t workspace_bytes, artemis_stream stream);
 
+/* ---- Training iteration bookkeeping (fit.py:474-501, :308-330) ---------
+ * artemis_l1_grads: dL/dF = sign(F - gt_F) / R, dL/dalpha = sign(alpha -
+ * gt_alpha) / R (F fp32 from artemis_forward_fit, the rest fp64), the
+ * per-ray loss term sum_c |dF| + |dalpha| into loss_rays and their ordered
+ * sum into *loss_sum (device). artemis_mark_touched: touched[row] = 1 for
+ * every hit (backward_batch's bitmap). artemis_vrt_grads: the collision
+ * pair term, grad[w] += s, grad[l] -= s with s = sign(data[w] - data[l]) *
+ * scale, applied per row in np.add.at's order; marks the rows touched.
+ * artemis_sparse_adam: SparseAdam.step on touched rows (bias1/bias2 =
+ * 1 - beta^t from the host), then the density clamp of those rows. */
+int artemis_l1_grads(const float *F, const double *alpha, const double *gt_F,
+                     const double *gt_alpha, int64_t n_rays, int channels, double *dldf,
+                     double *dlda, double *loss_rays, double *loss_sum, artemis_stream stream);
+int artemis_mark_touched(const int64_t *hit_idx, int64_t n_hits, uint8_t *touched,
+                         artemis_stream stream);
+size_t artemis_vrt_workspace_bytes(int64_t n_pairs, int64_t n_rows);
+int artemis_vrt_grads(const double *data, int64_t n_rows, int width, const int64_t *pairs,
+                      int64_t n_pairs, double scale, double *grad, uint8_t *touched,
+                      void *workspace, size_t workspace_bytes, artemis_stream stream);
+int artemis_sparse_adam(double *params, double *m, double *v, const double *grad,
+                        const uint8_t *touched, int64_t n_rows, int width, double lr,
+                        double beta1, double beta2, double eps, double bias1, double bias2,
+                        artemis_stream stream);
+
 /* Device ray generation (parity helper for rays_for_camera + _grid_rays).
  * og/dg/dw: (W*H, 3) fp64, row-major pixels. */
 int artemis_camera_rays(const artemis_camera *cam /* host */, double *og, double *dg,

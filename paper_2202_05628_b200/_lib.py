@@ -127,6 +127,11 @@ _SIGS = {
     "artemis_host_expand": (INT, [P, I64, INT, P, I64, P, P, P, P, INT]),
     "artemis_frame_bbox": (INT, [P, P, INT, INT, INT, P, P]),
     "artemis_copy_rect_d2h": (INT, [P, P, SZ, SZ, SZ, I64, I64, P]),
+    "artemis_l1_grads": (INT, [P, P, P, P, I64, INT, P, P, P, P, P]),
+    "artemis_mark_touched": (INT, [P, I64, P, P]),
+    "artemis_vrt_workspace_bytes": (SZ, [I64, I64]),
+    "artemis_vrt_grads": (INT, [P, I64, INT, P, I64, DBL, P, P, P, SZ, P]),
+    "artemis_sparse_adam": (INT, [P, P, P, P, P, I64, INT, DBL, DBL, DBL, DBL, DBL, DBL, P]),
     "artemis_tiles_shard_floats": (I64, [INT, INT, INT, INT, INT]),
     "artemis_tiles_pack": (INT, [P, P, P, INT, INT, INT, INT, INT, P, P]),
     "artemis_tiles_unpack": (INT, [P, INT, INT, INT, INT, INT, P, P, P, P]),

@@ -59,3 +59,8 @@ def golden_post():
 @pytest.fixture(scope="session")
 def golden_asset():
     return load_golden("asset")
+
+
+@pytest.fixture(scope="session")
+def golden_fit():
+    return load_golden("fit")

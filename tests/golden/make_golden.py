@@ -27,6 +27,8 @@ and registered as `animvox._core`) and records, on seeded inputs:
 * asset.npz        the .nvo container: digests of save_asset bytes and of
                    load_asset's arrays (rigged and unrigged 64^3 character),
                    and the exception class for each corrupted variant
+* fit.npz          the reference's SparseAdam steps, collision-pair term
+                   (np.add.at) and L1 sign gradients on seeded inputs
 * scene_c0.npz     configs[0] at full size (128^3, 256^2): SHA-256 digests of
                    every exact array plus a pixel subsample of the maps
 * scene_c2.npz     configs[2] at full size (512^3, 1024^2, C = 32 through a
@@ -482,6 +484,52 @@ def asset_fixtures():
     return out
 
 
+def fit_fixtures():
+    """The reference's own training bookkeeping on seeded inputs: three
+    SparseAdam steps (fit.py:308-330) with FLUT.clamp_densities, the
+    collision-pair term through GradBuffer.add (np.add.at, repeated rows)
+    and the L1 sign gradients of fit.py:486-488."""
+    from animvox import fit as FIT
+
+    rng = np.random.default_rng(123)
+    n, width = 40, 28
+    params = rng.uniform(-1, 1, size=(n, width))
+    params[:, -1] = rng.uniform(0.0, 0.02, size=n)
+    cfg = FIT.FitConfig(learning_rate=0.05)
+    opt = FIT.SparseAdam(params.shape, cfg)
+    grads, touches = [], []
+    p = params.copy()
+    for step in range(3):
+        g = np.zeros_like(p)
+        touched = rng.uniform(size=n) < 0.5
+        g[touched] = rng.normal(size=(int(touched.sum()), width))
+        g[touched, -1] = np.abs(g[touched, -1]) * 5  # drive densities below zero
+        grads.append(g)
+        touches.append(touched)
+        opt.step(p, FIT.GradBuffer(values=g.copy(), touched=touched.copy()))
+        fl = V.FLUT.__new__(V.FLUT)
+        fl.data = p
+        V.FLUT.clamp_densities(fl)
+    pairs = rng.integers(0, n, size=(60, 2))
+    pairs[:10, 0] = 3  # repeated winners
+    gbuf = FIT.GradBuffer(values=np.zeros((n, width)), touched=np.zeros(n, bool))
+    s = np.sign(params[pairs[:, 0]] - params[pairs[:, 1]])
+    s *= 0.01 / (pairs.shape[0] * width)
+    gbuf.add(pairs[:, 0], s)
+    gbuf.add(pairs[:, 1], -s)
+    F = rng.normal(size=(50, 3)).astype(np.float32)
+    A = rng.uniform(size=50)
+    gt_f = np.where(rng.uniform(size=(50, 3)) < 0.2, F.astype(np.float64), rng.normal(size=(50, 3)))
+    gt_a = np.where(rng.uniform(size=50) < 0.2, A, rng.uniform(size=50))
+    n_p = 50
+    return dict(params0=params, grads=np.stack(grads), touches=np.stack(touches), params3=p,
+                m3=opt.m, v3=opt.v, pairs=pairs, vrt_grad=gbuf.values, vrt_touched=gbuf.touched,
+                F=F, A=A, gt_f=gt_f, gt_a=gt_a,
+                dldf=np.sign(F.astype(np.float64) - gt_f) / n_p,
+                dlda=np.sign(A - gt_a) / n_p,
+                loss=np.float64(FIT.loss_rgba(F, A, gt_f, gt_a)))
+
+
 def main(which):
     t = time.time()
     if "kernels" in which:
@@ -501,6 +549,9 @@ def main(which):
     if "asset" in which:
         np.savez_compressed(os.path.join(HERE, "asset.npz"), **asset_fixtures())
         print("asset.npz", time.time() - t)
+    if "fit" in which:
+        np.savez_compressed(os.path.join(HERE, "fit.npz"), **fit_fixtures())
+        print("fit.npz", time.time() - t)
     if "c0" in which:
         sc = S.make_scene("c0")
         np.savez_compressed(os.path.join(HERE, "scene_c0.npz"),
@@ -514,4 +565,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "asset", "c0", "c2"])
+    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "asset", "fit", "c0", "c2"])
