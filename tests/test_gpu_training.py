@@ -94,13 +94,11 @@ def test_trainer_equals_host_loop():
     trainer = DeviceTrainer(start, sc.degree, sc.channels, lambda_vrt=0.01)
     host = start.copy()
     opt = oracle.SparseAdam(host.shape, lr=0.05)
-    losses = []
     for it in range(4):
         pick = rng.integers(0, og.shape[0], size=2048)
         args = (og[pick], dg[pick], dw[pick])
         l_rgba, l_vrt = trainer.step(tree, *args, gtF[pick], gtA[pick], rj, tables.rot_inv,
                                      pairs=pairs)
-        losses.append(l_rgba)
         # host loop: same GPU forward / backward, the reference's bookkeeping
         f, a, off, hi, h0, h1 = K.forward_fit(*tree, *args, 0.0, np.inf, host, rj,
                                               tables.rot_inv, sc.degree, sc.channels)
@@ -112,4 +110,7 @@ def test_trainer_equals_host_loop():
         oracle.vrt_add(grad, touched, host, pairs, 0.01)
         opt.step(host, grad, touched)
         assert np.array_equal(trainer.data, host), it
-    assert losses[-1] < losses[0]
+        want = np.mean(np.sum(np.abs(f.astype(np.float32).astype(np.float64) - gtF[pick]), 1)
+                       + np.abs(a - gtA[pick]))  # loss_rgba, fit.py:52-68
+        assert abs(l_rgba - want) <= 1e-12 * want
+        assert l_vrt > 0.0
