@@ -238,6 +238,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                            (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * sizeof(FeatT))) +
                        kRenderWarps * 32 * kQCap) +
                    warp * 32 * kQCap;
+    // world directions of the lanes' rays (read by phase B1 for any lane's
+    // queued leaves): shared memory instead of three registers pairs
+    double *s_dw = reinterpret_cast<double *>(wm - warp * 32 * kQCap + kRenderWarps * 32 * kQCap);
     if (kMode != kCount)
         for (int i = lane; i < 32 * cp; i += 32) feat[i] = FeatT(0);
     const int64_t n_leaves = p.n_leaves_dev ? (int64_t)*p.n_leaves_dev : p.n_leaves;
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // per-lane ray state
     int64_t ray = -1;
     bool walking = false;  // DFS not exhausted
-    double og[3], dg[3], dw[3];
+    double og[3], dg[3];
     RayF rf;
     // exact cell walk state (kDDA): current cell, step signs, exact entry /
     // exit crossing per axis, the leaf AABB exit, the cached brick
@@ -281,15 +284,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     double t_end = 0.0;
     int cb[3] = {0, 0, 0}, cbid = -1;
     double cTb[3] = {0, 0, 0};
-    int aL[3] = {0, 0, 0}, aU[3] = {0, 0, 0};
-    if (kDDA) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            aL[a] = __ldg(p.bm.aabb + a);
-            aU[a] = __ldg(p.bm.aabb + 3 + a);
-        }
-    }
-    double T = 1.0, acc = 0.0, depth = CUDART_INF;
+    // transmittance chain (T, accumulated alpha, depth): touched once per
+    // round (phase B2) and at retirement, so it lives in shared memory
+    double *s_tad = s_dw + 3 * kRenderThreads + 3 * tid;
     int64_t hits = 0, trace_base = 0;
     int cur = kEnd, top = 0, nq = 0;
     int ovf[kStack - kSmemStack];
@@ -470,6 +467,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     };
     auto start_ray = [&](int64_t id) {
         ray = -1;
+        double dw[3];
         if (kCamera) {
             const artemis_camera &cam = *p.cam;
             const int64_t tile = tstart + (id >> 5) * tstride;
@@ -490,6 +488,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
         }
         if (ray < 0) return;
+        if (kMode != kCount)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) s_dw[3 * tid + a] = dw[a];
         rf.exact_only = false;
         rf.cmax = 0.0f;
 #pragma unroll
@@ -508,9 +509,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         rf.tmin_dn = __double2float_rd(p.t_min);
         rf.tmax_up = __double2float_ru(p.t_max);
         rf.tmax_dn = __double2float_rd(p.t_max);
-        T = 1.0;
-        acc = 0.0;
-        depth = CUDART_INF;
+        s_tad[0] = 1.0;
+        s_tad[1] = 0.0;
+        s_tad[2] = CUDART_INF;
         hits = 0;
         top = 0;
         nq = 0;
@@ -522,6 +523,12 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             // the clipped entry distance
             walking = false;
             if (!(n_leaves > 0 && p.t_min < p.t_max)) return;
+            int aL[3], aU[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                aL[a] = __ldg(p.bm.aabb + a);
+                aU[a] = __ldg(p.bm.aabb + 3 + a);
+            }
             double t0 = p.t_min, t1 = p.t_max;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -617,7 +624,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             for (int a = 0; a < 3; ++a) {
                 so[a] = __shfl_sync(0xffffffffu, og[a], src);
                 sd[a] = __shfl_sync(0xffffffffu, dg[a], src);
-                if (kMode != kCount) sw[a] = __shfl_sync(0xffffffffu, dw[a], src);
+                if (kMode != kCount) sw[a] = s_dw[3 * (wbase + src) + a];
             }
             if (has && kMode != kCount) {
                 const int qi = k * kRenderThreads + wbase + src;
@@ -655,6 +662,12 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         __syncwarp();
         ARTEMIS_PHASE(3);
         // ---- phase B2: sequential per-ray integration over own leaves
+        double T = 1.0, acc = 0.0, depth = CUDART_INF;
+        if (nq > 0 && kMode != kCount) {
+            T = s_tad[0];
+            acc = s_tad[1];
+            depth = s_tad[2];
+        }
         for (int k = 0; k < nq; ++k) {
             const int qi = k * kRenderThreads + tid;
             const uint32_t id = q_id[qi];
@@ -691,6 +704,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 cur = kEnd;
                 break;
             }
+        }
+        if (nq > 0 && kMode != kCount) {
+            s_tad[0] = T;
+            s_tad[1] = acc;
+            s_tad[2] = depth;
         }
         ARTEMIS_PHASE(4);
         // ---- phase C: shade the visible queued leaves level by level (a ray
@@ -815,6 +833,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         ARTEMIS_PHASE(5);
         // ---- retire finished rays: scalars per lane, features row by row
         const bool done = ray >= 0 && !walking;
+        if (kMode != kCount && done) {
+            acc = s_tad[1];
+            depth = s_tad[2];
+        }
         if (done) {
             if (kMode == kCount) {
                 p.counts[ray] = hits;
@@ -857,7 +879,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     const size_t feat_bytes = 4;
     const size_t smem = stack_bytes(kDDA) + queue_bytes(kRays == 1) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * feat_bytes) +
-                        (size_t)kRenderWarps * 32 * kQCap * (2 + 4);
+                        (size_t)kRenderWarps * 32 * kQCap * (2 + 4) + (size_t)kRenderThreads * 6 * 8;
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
