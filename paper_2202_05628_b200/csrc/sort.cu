@@ -8,12 +8,13 @@
 //
 // Tile = 8 warps x 16 items x 32 lanes = 4096 keys. Warp w owns the
 // contiguous 512-key chunk w of the tile and walks it in 16 coalesced rows;
-// ranks are built row by row with __match_any_sync so the (warp, row, lane)
+// ranks are built row by row (peer lanes from 8 bit-plane ballots) so the (warp, row, lane)
 // order -- i.e. input order -- is preserved inside each digit. Thread d of
 // the CTA then owns digit d: it prefixes the 8 warp counts, publishes the
 // tile aggregate, and walks back over earlier tiles' published values
 // (flag in the top 2 bits of one 32-bit word: 0 = pending, 1 = aggregate,
-// 2 = inclusive prefix) until it meets an inclusive prefix.
+// 2 = inclusive prefix) until it meets an inclusive prefix, reading the
+// statuses of kLook predecessors per memory round trip.
 #include "common.cuh"
 #include "tree.cuh"
 
@@ -27,6 +28,7 @@ constexpr int kTile = kThreads * kItems;
 constexpr int kWarpTile = 32 * kItems;
 constexpr int kRadix = 256;
 constexpr uint32_t kValMask = (1u << 30) - 1;
+constexpr int kLook = 32;  // look-back window (tiles whose status is read at once)
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -107,6 +109,11 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     __shared__ uint32_t s_tile;
     __shared__ uint32_t whist[kWarps][kRadix];
     __shared__ uint32_t dbase[kRadix];
+    __shared__ uint32_t tpre[kRadix];   // tile-local exclusive prefix per digit
+    __shared__ uint32_t wsum[kWarps];
+    extern __shared__ __align__(16) unsigned char s_stage[];  // tile reordered by digit
+    K *skey = reinterpret_cast<K *>(s_stage);
+    uint32_t *sval = reinterpret_cast<uint32_t *>(s_stage + kTile * sizeof(K));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int i = tid; i < kWarps * kRadix; i += kThreads) (&whist[0][0])[i] = 0;
@@ -129,9 +136,17 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     for (int j = 0; j < kItems; ++j) {
         int64_t idx = base + j * 32 + lane;
         unsigned valid = __ballot_sync(0xffffffffu, idx < n);
+        // lanes holding the same digit: 8 bit-plane ballots (cheaper than
+        // __match_any_sync when a row holds many distinct digits)
+        const uint32_t dj = (uint32_t)((key[j] >> shift) & 0xFF);
+        unsigned peers = valid;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const unsigned bb = __ballot_sync(0xffffffffu, (dj >> b) & 1u);
+            peers &= ((dj >> b) & 1u) ? bb : ~bb;
+        }
         if (idx < n) {
-            uint32_t d = (uint32_t)((key[j] >> shift) & 0xFF);
-            unsigned peers = __match_any_sync(valid, d);
+            uint32_t d = dj;
             uint32_t prev = whist[warp][d];
             __syncwarp(valid);
             if (lane == __ffs(peers) - 1) whist[warp][d] = prev + __popc(peers);
@@ -140,43 +155,78 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
         }
     }
     __syncthreads();
-    {
-        const int d = tid;  // kThreads == kRadix: thread d owns digit d
-        uint32_t tot = 0;
+    const int d = tid;  // kThreads == kRadix: thread d owns digit d
+    uint32_t tot = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            uint32_t x = whist[w][d];
-            whist[w][d] = tot;
-            tot += x;
+    for (int w = 0; w < kWarps; ++w) {
+        uint32_t x = whist[w][d];
+        whist[w][d] = tot;
+        tot += x;
+    }
+    uint32_t *mine = status + tile * kRadix + d;
+    // publish this tile's aggregate first: later tiles sum it while this one
+    // stages its keys and looks back
+    st_relaxed(mine, (tile == 0 ? 2u << 30 : 1u << 30) | tot);
+    {   // tile-local digit offsets (block exclusive scan of the counts)
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        uint32_t *mine = status + tile * kRadix + d;
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_relaxed(mine, (2u << 30) | tot);
-        } else {
-            st_relaxed(mine, (1u << 30) | tot);
-            for (int64_t k = tile - 1;;) {
-                uint32_t s = ld_relaxed(status + k * kRadix + d);
-                uint32_t flag = s >> 30;
-                if (flag == 0) continue;
-                excl += s & kValMask;
-                if (flag == 2) break;
-                --k;
-            }
-            st_relaxed(mine, (2u << 30) | (excl + tot));
-        }
-        dbase[d] = digit_offsets[d] + excl;
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += wsum[w];
+        tpre[d] = wpre + x - tot;
     }
     __syncthreads();
+    // stage the tile in digit order (frees the key/value registers for the
+    // look-back); each digit's run is written out with consecutive threads
+    // on consecutive addresses below
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
         int64_t idx = base + j * 32 + lane;
         if (idx < n) {
-            uint32_t d = (uint32_t)((key[j] >> shift) & 0xFF);
-            uint32_t pos = dbase[d] + whist[warp][d] + rank[j];
-            kout[pos] = key[j];
-            vout[pos] = val[j];
+            uint32_t dd = (uint32_t)((key[j] >> shift) & 0xFF);
+            uint32_t lp = tpre[dd] + whist[warp][dd] + rank[j];
+            skey[lp] = key[j];
+            sval[lp] = val[j];
         }
+    }
+    {
+        uint32_t excl = 0;
+        if (tile > 0) {
+            // look back kLook predecessors at a time: their statuses are
+            // loaded together (one memory round trip per window, not per
+            // tile -- every tile of a small sort is resident at once, so
+            // the walk back can be long), then consumed nearest first
+            bool done = false;
+            for (int64_t k = tile - 1; !done; k -= kLook) {
+                uint32_t w[kLook];
+#pragma unroll
+                for (int i = 0; i < kLook; ++i)
+                    w[i] = k - i >= 0 ? ld_relaxed(status + (k - i) * kRadix + d) : (2u << 30);
+#pragma unroll
+                for (int i = 0; i < kLook; ++i) {
+                    if (done) break;
+                    uint32_t sv = w[i];
+                    while ((sv >> 30) == 0) sv = ld_relaxed(status + (k - i) * kRadix + d);
+                    excl += sv & kValMask;
+                    if ((sv >> 30) == 2) done = true;
+                }
+            }
+            st_relaxed(mine, (2u << 30) | (excl + tot));
+        }
+        dbase[d] = digit_offsets[d] + excl - tpre[d];
+    }
+    __syncthreads();
+    const int tile_n = (int)std::min<int64_t>(kTile, n - tile * kTile);
+    for (int i = tid; i < tile_n; i += kThreads) {
+        const K k = skey[i];
+        const uint32_t pos = dbase[(uint32_t)((k >> shift) & 0xFF)] + (uint32_t)i;
+        kout[pos] = k;
+        vout[pos] = sval[i];
     }
 }
 
@@ -204,6 +254,13 @@ int sort_pairs(const K *keys_in, const uint32_t *vals_in, K *keys_out, uint32_t 
                                              (int64_t)num_sms() * 4);
     radix_hist_kernel<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n, L.passes, hist);
     radix_scan_kernel<<<L.passes, kRadix, 0, st>>>(hist);
+    const size_t stage = (size_t)kTile * (sizeof(K) + 4);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(onesweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+        cudaFuncSetAttribute(onesweep_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+        attr_set = true;
+    }
     const K *src_k = keys_in;
     const uint32_t *src_v = vals_in;
     for (int p = 0; p < L.passes; ++p) {
@@ -212,10 +269,10 @@ int sort_pairs(const K *keys_in, const uint32_t *vals_in, K *keys_out, uint32_t 
         uint32_t *dv = to_out ? vals_out : alt_v;
         uint32_t *stp = status + (size_t)p * L.tiles * kRadix;
         if (p == 0 && !vals_in)
-            onesweep_kernel<K, true><<<(int)L.tiles, kThreads, 0, st>>>(
+            onesweep_kernel<K, true><<<(int)L.tiles, kThreads, stage, st>>>(
                 src_k, nullptr, dk, dv, n, 8 * p, hist + p * kRadix, stp, counters + p);
         else
-            onesweep_kernel<K, false><<<(int)L.tiles, kThreads, 0, st>>>(
+            onesweep_kernel<K, false><<<(int)L.tiles, kThreads, stage, st>>>(
                 src_k, src_v, dk, dv, n, 8 * p, hist + p * kRadix, stp, counters + p);
         src_k = dk;
         src_v = dv;

@@ -1,4 +1,3 @@
 cd "$GRAFT_REPO_ROOT"
-timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "Crossing" 2>&1 | tail -3
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -3
-timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['stage_ms'])"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:onesweep -s 5 -c 1 -o gpurun_out/prof_sort python scripts/prof_frame.py c2 2 > gpurun_out/ncu_sort.log 2>&1
+echo rc=$?
