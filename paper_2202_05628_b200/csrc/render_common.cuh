@@ -1,6 +1,6 @@
-// Pieces shared by the render kernels (render.cu: all modes; render_ws.cu:
-// the warp-specialised camera kernel): launch arguments, the exact camera
-// ray, the fp32 SH basis, an L2 prefetch.
+// Pieces shared by the render kernels (render.cu, all modes) and the
+// gradient kernels: launch arguments, the exact camera ray, the fp32 SH
+// basis, an L2 prefetch.
 #pragma once
 #include <math.h>
 
