@@ -1,0 +1,123 @@
+"""Edge cases of the device frame pipeline against the CPU oracle (which is
+pinned to the reference by tests/test_oracle_golden.py): image sizes that
+are not whole 8x4 tiles, a single pixel, a camera inside the body's box,
+rays running exactly along grid planes (zero direction components, origins
+on a plane), a one-voxel character, and the exact tree arrays the rebuild
+leaves behind in each case. Same bars as the other parity tests: tree and
+depth exact, F within 1e-4 max / 1e-5 mean-abs, alpha within 1e-6 (fp32
+maps) or 1e-9 (fp64 maps, ARTEMIS_FRAME_MAPS64)."""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2202_05628_b200 import kinematics as KM
+from paper_2202_05628_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+F_MAX, F_MEAN = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module")
+def mini():
+    return S.make_scene("c0", resolution=64, image=(64, 64))
+
+
+def frame_vs_oracle(sc, pose, cam, maps64=False, graph=False):
+    from paper_2202_05628_b200.frame import FramePipeline
+
+    fp = FramePipeline.from_scene(sc)
+    try:
+        F, A, D = fp.run(pose, cam, graph=graph, parity=True, maps64=maps64,
+                         lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep)
+        fp.stream.synchronize()
+        if pose is not None:
+            want = oracle.render_frame(sc, KM.pose_tables(sc.rig, pose), cam)
+        else:  # canonical cells, rotation joint 0, identity inverse rotation
+            tree = oracle.build_octree(sc.cells)
+            R, origin = cam.cam_to_world()
+            og, dg, dw = oracle.camera_rays(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
+                                            cam.height, sc.lo, sc.cell_size)
+            Fw, Aw, Dw = oracle.render_rays(*tree, og, dg, dw, 0.0, np.inf, sc.flut64(),
+                                            np.zeros(sc.n_voxels, np.int32),
+                                            KM.identity_tables().rot_inv, sc.degree, sc.channels,
+                                            sc.lambda_th, sc.sigma_dep, True)
+            want = dict(tree=tree, F=Fw, A=Aw, D=Dw)
+        codes, fidx, root, left, right, bmin, bsize = want["tree"]
+        t = fp.tree()
+        assert t["n_live"] == codes.size
+        assert np.array_equal(t["codes"], codes) and np.array_equal(t["flut_idx"], fidx)
+        assert t["root"] == root
+        for k, v in (("left", left), ("right", right), ("box_min", bmin), ("box_size", bsize)):
+            assert np.array_equal(t[k], v), k
+        Fh = F.cpu().numpy().astype(np.float64)
+        err = np.abs(Fh - want["F"])
+        assert err.max(initial=0.0) <= F_MAX and err.mean() <= F_MEAN
+        Ah, Dh = A.cpu().numpy(), D.cpu().numpy()
+        if maps64:
+            assert np.max(np.abs(Ah - want["A"]), initial=0.0) <= 1e-9
+            assert np.array_equal(Dh, want["D"])
+        else:
+            assert np.max(np.abs(Ah - want["A"]), initial=0.0) <= 1e-6
+            assert np.array_equal(Dh, want["D"].astype(np.float32))
+        return want
+    finally:
+        fp.close()
+
+
+@pytest.mark.parametrize("size", [(37, 23), (1, 1), (9, 5), (8, 4)])
+def test_image_not_whole_tiles(mini, size):
+    W, H = size
+    cam = KM.orbit(math.radians(30.0), math.radians(10.0), 2.5, W, H,
+                   KM.focal_for_fov(max(W, 8), 40.0))
+    frame_vs_oracle(mini, KM.PoseSpec.make(mini.poses[0]), cam)
+
+
+@pytest.mark.parametrize("maps64", [False, True])
+def test_camera_inside_the_body_box(mini, maps64):
+    """Rays start inside the leaf AABB (the walk's first cell comes from the
+    origin, not from an AABB entry)."""
+    cam = KM.look_at([0.05, -0.03, 0.02], [1.0, 0.3, 0.1], 48, 40, KM.focal_for_fov(48, 90.0))
+    want = frame_vs_oracle(mini, KM.PoseSpec.make(mini.poses[0]), cam, maps64=maps64)
+    assert (want["A"] > 0).any()
+
+
+def test_rays_along_grid_planes(mini):
+    """Camera on the x axis looking down -x with an odd image: the centre
+    column/row rays have exactly zero y/z direction components and grid
+    origins exactly on cell planes (og = 32), the slab test's d == 0
+    branch; every other ray crosses planes at exactly tied distances
+    along the image diagonals."""
+    cam = KM.look_at([2.5, 0.0, 0.0], [0.0, 0.0, 0.0], 33, 33, KM.focal_for_fov(33, 40.0))
+    R, origin = cam.cam_to_world()
+    og, dg, dw = oracle.camera_rays(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
+                                    cam.height, mini.lo, mini.cell_size)
+    assert (dg[:, 1] == 0.0).any() and (dg[:, 2] == 0.0).any()
+    assert og[0, 1] == np.floor(og[0, 1])
+    want = frame_vs_oracle(mini, None, cam)
+    assert (want["A"] > 0).any()
+
+
+def test_axis_aligned_camera_posed(mini):
+    cam = KM.look_at([0.0, -2.5, 0.0], [0.0, 0.0, 0.0], 33, 31, KM.focal_for_fov(33, 40.0))
+    frame_vs_oracle(mini, KM.PoseSpec.make(mini.poses[0]), cam, graph=True)
+
+
+def test_single_voxel_character(mini):
+    """One voxel: the tree is the lone leaf (root = ~0, no internal nodes)."""
+    i = mini.n_voxels // 2
+    sc = dataclasses.replace(mini, cells=mini.cells[i:i + 1].copy(),
+                             flut32=mini.flut32[i:i + 1].copy(),
+                             skin_idx=mini.skin_idx[i:i + 1].copy(),
+                             skin_w=mini.skin_w[i:i + 1].copy())
+    c = sc.centers()[0]
+    cam = KM.look_at(c + np.array([0.0, -1.0, 0.0]), c, 17, 17, KM.focal_for_fov(17, 5.0))
+    want = frame_vs_oracle(sc, None, cam)
+    assert want["tree"][2] == ~0
+    assert (want["A"] > 0).any()
