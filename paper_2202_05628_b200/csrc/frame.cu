@@ -14,6 +14,10 @@
 // pose- and camera-independent.
 #include <string.h>
 
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
 #include "bricks.cuh"
 #include "common.cuh"
 #include "tree.cuh"
@@ -28,7 +32,8 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
-                  void *A, void *D, unsigned long long *queue, cudaStream_t st);
+                  void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
+                  cudaStream_t st);
 
 constexpr int kMaxFrameJoints = 256;
 
@@ -81,6 +86,14 @@ struct artemis_frame_s {
     };
     static constexpr int kGraphSlots = 4;
     GraphSlot graphs[kGraphSlots];
+    // render order of the 8x4 tiles per image size: centre out (see
+    // tile_order_for); a few sizes cached, like the graphs
+    struct OrderSlot {
+        int w = 0, h = 0;
+        int32_t *dev = nullptr;
+        unsigned long long used = 0;
+    };
+    OrderSlot orders[kGraphSlots];
     unsigned long long graph_clock = 0;
     int launches = 0;
     // stage profiling (eager runs only): events before warp, sort, resolve,
@@ -103,7 +116,7 @@ int dev_alloc(T **p, size_t bytes) {
 
 int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int height,
                   int sharded, double lambda_th, double sigma_dep, int flags, float *F, void *A,
-                  void *D, cudaStream_t st) {
+                  void *D, const int32_t *order, cudaStream_t st) {
     const artemis_asset &as = f->asset;
     int rc;
     int launches = 0;
@@ -121,7 +134,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            as.channels, 0};
         rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th,
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
-                           reinterpret_cast<unsigned long long *>(f->counters + 2), st);
+                           reinterpret_cast<unsigned long long *>(f->counters + 2), order, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -189,13 +202,66 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                        as.channels, 0};
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
                        flags & 1, (flags & 8) ? 1 : 0, F, A, D,
-                       reinterpret_cast<unsigned long long *>(f->counters + 2), st);
+                       reinterpret_cast<unsigned long long *>(f->counters + 2), order, st);
     mark(5);
     launches += 1;
     f->launches = launches;
     return rc;
 }
 
+}  // namespace
+
+namespace {
+// Render order of an image's 8x4 tiles: by distance of the tile centre from
+// the image centre (ties in row-major order). The render kernel's rays come
+// off a queue in this order, so the expensive middle of a framed character
+// starts first and the cheap border tiles fill the tail (measured at
+// configs[2]: 1.65 -> 1.54 ms against row-major; any order gives the same
+// maps bit for bit -- each ray is independent and its own sums keep hit
+// order). Cached per image size next to the graphs that capture it.
+int tile_order_for(artemis_frame f, int w, int h, const int32_t **out) {
+    artemis_frame_s::OrderSlot *slot = nullptr, *victim = &f->orders[0];
+    for (auto &o : f->orders) {
+        if (o.dev && o.w == w && o.h == h) {
+            slot = &o;
+            break;
+        }
+        if (!o.dev || (victim->dev && o.used < victim->used)) victim = &o;
+    }
+    if (!slot) {
+        slot = victim;
+        if (slot->dev) {  // graphs captured for that size read the old buffer
+            for (auto &g : f->graphs)
+                if (g.exec && g.w == slot->w && g.h == slot->h) {
+                    cudaGraphExecDestroy(g.exec);
+                    g.exec = nullptr;
+                }
+            cudaFree(slot->dev);
+            slot->dev = nullptr;
+        }
+        const int tx = (w + 7) / 8, ty = (h + 3) / 4;
+        const int64_t n = (int64_t)tx * ty;
+        std::vector<int32_t> idx((size_t)n);
+        std::vector<double> key((size_t)n);
+        std::iota(idx.begin(), idx.end(), 0);
+        for (int64_t t = 0; t < n; ++t) {
+            const double dx = (double)(t % tx) * 8.0 + 4.0 - 0.5 * w;
+            const double dy = (double)(t / tx) * 4.0 + 2.0 - 0.5 * h;
+            key[(size_t)t] = dx * dx + dy * dy;
+        }
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int32_t a, int32_t b) { return key[(size_t)a] < key[(size_t)b]; });
+        int rc = dev_alloc(&slot->dev, (size_t)n * sizeof(int32_t));
+        if (rc) return rc;
+        ARTEMIS_TRY(cudaMemcpy(slot->dev, idx.data(), (size_t)n * sizeof(int32_t),
+                               cudaMemcpyHostToDevice));
+        slot->w = w;
+        slot->h = h;
+    }
+    slot->used = ++f->graph_clock;
+    *out = slot->dev;
+    return ARTEMIS_OK;
+}
 }  // namespace
 
 extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) {
@@ -278,6 +344,8 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     for (cudaEvent_t e : f->staged)
         if (e) cudaEventDestroy(e);
     if (f->staging) cudaFreeHost(f->staging);
+    for (auto &o : f->orders)
+        if (o.dev) cudaFree(o.dev);
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
                     f->leaves, f->btable, f->brecs, f->bmeta,
@@ -322,10 +390,15 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
     }
     ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));
     const int sharded = cam->tile_stride > 1;
+    const int32_t *order = nullptr;
+    if (!sharded) {
+        int rc = tile_order_for(f, cam->width, cam->height, &order);
+        if (rc) return rc;
+    }
     const int use_graph = (flags & 2) && st != nullptr;
     if (!use_graph)
         return enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded, lambda_th,
-                             sigma_dep, flags, F, alpha, depth, st);
+                             sigma_dep, flags, F, alpha, depth, order, st);
     artemis_frame_s::GraphSlot *slot = nullptr, *victim = &f->graphs[0];
     for (auto &g : f->graphs) {
         if (g.exec && g.w == cam->width && g.h == cam->height && g.flags == flags &&
@@ -345,7 +418,7 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
         }
         ARTEMIS_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         int rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded,
-                               lambda_th, sigma_dep, flags, F, alpha, depth, st);
+                               lambda_th, sigma_dep, flags, F, alpha, depth, order, st);
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(st, &g);
         if (rc) {

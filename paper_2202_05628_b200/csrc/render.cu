@@ -470,7 +470,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         double dw[3];
         if (kCamera) {
             const artemis_camera &cam = *p.cam;
-            const int64_t tile = tstart + (id >> 5) * tstride;
+            const int64_t t = tstart + (id >> 5) * tstride;
+            const int64_t tile = p.tile_order ? (int64_t)__ldg(p.tile_order + t) : t;
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
             const int py = (int)(tile / p.tiles_x) * 4 + (sl >> 3);
@@ -966,8 +967,10 @@ __global__ void fill_alpha_depth(T *A, T *D, int64_t n) {
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
-                  void *A, void *D, unsigned long long *queue, cudaStream_t st) {
+                  void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
+                  cudaStream_t st) {
     RenderArgs a{};
+    a.tile_order = sharded ? nullptr : tile_order;
     fill_tree(a, tree);
     fill_shade(a, shade);
     a.cam = cam_dev;

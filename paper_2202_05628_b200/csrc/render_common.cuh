@@ -33,6 +33,7 @@ struct RenderArgs {
     int64_t n_rays;
     int tiles_x, tiles_y;  // camera mode: ceil(W / 8), ceil(H / 4)
     unsigned long long *queue;  // ray-id counter, zero at launch
+    const int32_t *tile_order;  // camera mode, unsharded: the i-th 8x4 tile to visit (a permutation)
     double t_min, t_max;
     double stop;  // 1 - lambda_th
     float coord_max;  // upper bound of every box coordinate (grid resolution)
