@@ -331,6 +331,15 @@ int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double
                       double sigma_dep, int flags, float *F, void *alpha, void *depth,
                       artemis_stream stream);
 
+/* Render order of the 8x4 ray tiles for one image size: `order` (HOST,
+ * ceil(w/8)*ceil(h/4) int32) must be a permutation of the tile indices
+ * (row-major tile numbering); ARTEMIS_ERR_ARG otherwise. Without it the
+ * pipeline times row-major and centre-out on the first frame of each size
+ * and keeps the faster (ARTEMIS_TILE_ORDER=rowmajor|centre forces one).
+ * The order never changes the maps: every ray is rendered independently. */
+int artemis_frame_set_tile_order(artemis_frame frame, int width, int height,
+                                 const int32_t *order);
+
 /* Read back the last frame's counts (synchronises the stream). */
 int artemis_frame_counts(artemis_frame frame, int64_t *n_in_bounds, int64_t *n_live,
                          artemis_stream stream);

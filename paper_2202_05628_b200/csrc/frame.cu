@@ -14,7 +14,10 @@
 // pose- and camera-independent.
 #include <string.h>
 
+#include <math.h>
+
 #include <algorithm>
+#include <string>
 #include <numeric>
 #include <vector>
 
@@ -87,10 +90,11 @@ struct artemis_frame_s {
     static constexpr int kGraphSlots = 4;
     GraphSlot graphs[kGraphSlots];
     // render order of the 8x4 tiles per image size: centre out (see
-    // tile_order_for); a few sizes cached, like the graphs
+    // order_slot); a few sizes cached, like the graphs
     struct OrderSlot {
         int w = 0, h = 0;
         int32_t *dev = nullptr;
+        int mode = -1;  // -1 not yet calibrated, 0 row-major, 1 centre-out (dev)
         unsigned long long used = 0;
     };
     OrderSlot orders[kGraphSlots];
@@ -212,14 +216,18 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
 }  // namespace
 
 namespace {
-// Render order of an image's 8x4 tiles: by distance of the tile centre from
-// the image centre (ties in row-major order). The render kernel's rays come
-// off a queue in this order, so the expensive middle of a framed character
-// starts first and the cheap border tiles fill the tail (measured at
-// configs[2]: 1.65 -> 1.54 ms against row-major; any order gives the same
-// maps bit for bit -- each ray is independent and its own sums keep hit
-// order). Cached per image size next to the graphs that capture it.
-int tile_order_for(artemis_frame f, int w, int h, const int32_t **out) {
+// Render order of an image's 8x4 ray tiles. Two candidates: row-major
+// (nullptr) and centre-out (by distance of the tile centre from the image
+// centre, ties row-major), which starts a framed character's expensive
+// middle first so the cheap border fills the tail. Which one is faster
+// depends on the asset and view (measured: configs[2] 1.78 -> 1.72 ms and
+// configs[1] 2.26 -> 2.19 ms with centre-out, configs[4] 9.5 -> 10.9 ms),
+// so the first frame of each image size times both (calibrate_order) and
+// keeps the faster. Any order gives the same maps bit for bit: each ray is
+// independent and its own sums keep hit order. Cached per image size next
+// to the graphs that capture the choice.
+artemis_frame_s::OrderSlot *order_slot(artemis_frame f, int w, int h, int *rc) {
+    *rc = ARTEMIS_OK;
     artemis_frame_s::OrderSlot *slot = nullptr, *victim = &f->orders[0];
     for (auto &o : f->orders) {
         if (o.dev && o.w == w && o.h == h) {
@@ -251,18 +259,50 @@ int tile_order_for(artemis_frame f, int w, int h, const int32_t **out) {
         }
         std::stable_sort(idx.begin(), idx.end(),
                          [&](int32_t a, int32_t b) { return key[(size_t)a] < key[(size_t)b]; });
-        int rc = dev_alloc(&slot->dev, (size_t)n * sizeof(int32_t));
-        if (rc) return rc;
-        ARTEMIS_TRY(cudaMemcpy(slot->dev, idx.data(), (size_t)n * sizeof(int32_t),
-                               cudaMemcpyHostToDevice));
+        *rc = dev_alloc(&slot->dev, (size_t)n * sizeof(int32_t));
+        if (*rc) return nullptr;
+        if (cudaMemcpy(slot->dev, idx.data(), (size_t)n * sizeof(int32_t),
+                       cudaMemcpyHostToDevice) != cudaSuccess) {
+            *rc = ARTEMIS_ERR_CUDA;
+            return nullptr;
+        }
         slot->w = w;
         slot->h = h;
+        slot->mode = -1;
+        const char *e = getenv("ARTEMIS_TILE_ORDER");  // "rowmajor" / "centre" force one
+        if (e && !strcmp(e, "rowmajor")) slot->mode = 0;
+        if (e && !strcmp(e, "centre")) slot->mode = 1;
     }
     slot->used = ++f->graph_clock;
-    *out = slot->dev;
-    return ARTEMIS_OK;
+    return slot;
 }
 }  // namespace
+
+// Install a caller-supplied render order (a permutation of the w x h image's
+// 8x4 tiles, host array) for that image size; graphs captured for the size
+// are dropped.
+extern "C" int artemis_frame_set_tile_order(artemis_frame f, int w, int h, const int32_t *order) {
+    if (!f || w < 1 || h < 1 || !order) return ARTEMIS_ERR_ARG;
+    int rc = ARTEMIS_OK;
+    artemis_frame_s::OrderSlot *slot = order_slot(f, w, h, &rc);
+    if (!slot) return rc;
+    const int32_t *dev = slot->dev;
+    slot->mode = 1;
+    const int64_t n = (int64_t)((w + 7) / 8) * ((h + 3) / 4);
+    std::vector<char> seen((size_t)n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (order[i] < 0 || order[i] >= n || seen[(size_t)order[i]]) return ARTEMIS_ERR_ARG;
+        seen[(size_t)order[i]] = 1;
+    }
+    for (auto &g : f->graphs)
+        if (g.exec && g.w == w && g.h == h) {
+            cudaGraphExecDestroy(g.exec);
+            g.exec = nullptr;
+        }
+    ARTEMIS_TRY(cudaMemcpy(const_cast<int32_t *>(dev), order, (size_t)n * sizeof(int32_t),
+                           cudaMemcpyHostToDevice));
+    return ARTEMIS_OK;
+}
 
 extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) {
     if (!a || !out || a->n_voxels < 1 || a->n_voxels >= (int64_t(1) << 30) || a->slots < 1 ||
@@ -293,6 +333,7 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->winners, n * 4);
     rc = rc ? rc : dev_alloc(&f->rot_joint, n * 4);
     rc = rc ? rc : dev_alloc(&f->counters, 64);
+    if (!rc && cudaMemset(f->counters, 0, 64) != cudaSuccess) rc = ARTEMIS_ERR_CUDA;
     rc = rc ? rc : dev_alloc(&f->left, n * 4);
     rc = rc ? rc : dev_alloc(&f->right, n * 4);
     rc = rc ? rc : dev_alloc(&f->bmin, n * 12);
@@ -392,8 +433,34 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
     const int sharded = cam->tile_stride > 1;
     const int32_t *order = nullptr;
     if (!sharded) {
-        int rc = tile_order_for(f, cam->width, cam->height, &order);
-        if (rc) return rc;
+        int rc = ARTEMIS_OK;
+        artemis_frame_s::OrderSlot *slot = order_slot(f, cam->width, cam->height, &rc);
+        if (!slot) return rc;
+        if (slot->mode < 0) {
+            // first frame of this size: time this frame's full pipeline with
+            // each order (eager, twice each, best of two) and keep the faster
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            ARTEMIS_TRY(cudaEventCreate(&e0));
+            ARTEMIS_TRY(cudaEventCreate(&e1));
+            float best[2] = {1e30f, 1e30f};
+            for (int rep = 0; rep < 2 && !rc; ++rep)
+                for (int m = 0; m < 2 && !rc; ++m) {
+                    cudaEventRecord(e0, st);
+                    rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, 0,
+                                       lambda_th, sigma_dep, flags & ~2, F, alpha, depth,
+                                       m ? slot->dev : nullptr, st);
+                    cudaEventRecord(e1, st);
+                    float ms = 0.0f;
+                    if (!rc && cudaEventSynchronize(e1) == cudaSuccess &&
+                        cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < best[m])
+                        best[m] = ms;
+                }
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            if (rc) return rc;
+            slot->mode = best[1] < best[0] ? 1 : 0;
+        }
+        order = slot->mode ? slot->dev : nullptr;
     }
     const int use_graph = (flags & 2) && st != nullptr;
     if (!use_graph)

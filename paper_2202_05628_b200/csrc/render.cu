@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         tstride = p.cam->tile_stride;
     }
     const int64_t n_tiles = (int64_t)p.tiles_x * p.tiles_y;
+    const int32_t *order = kCamera ? p.tile_order : nullptr;
     const int64_t n_ids = kCamera ? (tstart < n_tiles ? (n_tiles - tstart + tstride - 1) / tstride : 0) * 32
                                   : p.n_rays;
     const unsigned lt = lanemask_lt();
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         if (kCamera) {
             const artemis_camera &cam = *p.cam;
             const int64_t t = tstart + (id >> 5) * tstride;
-            const int64_t tile = p.tile_order ? (int64_t)__ldg(p.tile_order + t) : t;
+            const int64_t tile = order ? (int64_t)__ldg(order + t) : t;
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
             const int py = (int)(tile / p.tiles_x) * 4 + (sl >> 3);

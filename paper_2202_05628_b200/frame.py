@@ -439,6 +439,13 @@ class FramePipeline:
         out["root"] = 0 if n_live > 1 else ~0
         return out
 
+    def set_tile_order(self, width: int, height: int, order) -> None:
+        """Render the 8x4 ray tiles of a width x height image in `order` (a
+        permutation of the row-major tile indices); the maps do not change."""
+        o = np.ascontiguousarray(order, dtype=np.int32)
+        check(_lib.lib().artemis_frame_set_tile_order(self._h, int(width), int(height),
+                                                      o.ctypes.data), "frame_set_tile_order")
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.lib().artemis_frame_destroy(self._h)
