@@ -334,8 +334,8 @@ int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double
 /* Render order of the 8x4 ray tiles for one image size: `order` (HOST,
  * ceil(w/8)*ceil(h/4) int32) must be a permutation of the tile indices
  * (row-major tile numbering); ARTEMIS_ERR_ARG otherwise. Without it the
- * pipeline times row-major and centre-out on the first frame of each size
- * and keeps the faster (ARTEMIS_TILE_ORDER=rowmajor|centre forces one).
+ * pipeline renders centre-out while the asset's FLUT coefficients fit in
+ * 16x L2, row-major beyond (ARTEMIS_TILE_ORDER=rowmajor|centre forces one).
  * The order never changes the maps: every ray is rendered independently. */
 int artemis_frame_set_tile_order(artemis_frame frame, int width, int height,
                                  const int32_t *order);

@@ -36,12 +36,14 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
-                  cudaStream_t st);
+                  const int32_t *order_on, cudaStream_t st);
 
 constexpr int kMaxFrameJoints = 256;
 
 struct FrameParams {
     artemis_camera cam;
+    int32_t order_on;  // render the ray tiles in the size's centre-out order (else row-major)
+    int32_t pad;
     double aff[kMaxFrameJoints * 12];
     double rot_inv[kMaxFrameJoints * 9];
 };
@@ -89,15 +91,16 @@ struct artemis_frame_s {
     };
     static constexpr int kGraphSlots = 4;
     GraphSlot graphs[kGraphSlots];
-    // render order of the 8x4 tiles per image size: centre out (see
-    // order_slot); a few sizes cached, like the graphs
+    // render order of the 8x4 tiles per image size (see order_slot); a few
+    // sizes cached, like the graphs
     struct OrderSlot {
         int w = 0, h = 0;
         int32_t *dev = nullptr;
-        int mode = -1;  // -1 not yet calibrated, 0 row-major, 1 centre-out (dev)
+        int mode = 0;  // 0 row-major, 1 the order in dev (centre-out or set_tile_order)
         unsigned long long used = 0;
     };
     OrderSlot orders[kGraphSlots];
+
     unsigned long long graph_clock = 0;
     int launches = 0;
     // stage profiling (eager runs only): events before warp, sort, resolve,
@@ -138,7 +141,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            as.channels, 0};
         rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th,
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
-                           reinterpret_cast<unsigned long long *>(f->counters + 2), order, st);
+                           reinterpret_cast<unsigned long long *>(f->counters + 2), order,
+                           &f->params->order_on, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -206,7 +210,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                        as.channels, 0};
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
                        flags & 1, (flags & 8) ? 1 : 0, F, A, D,
-                       reinterpret_cast<unsigned long long *>(f->counters + 2), order, st);
+                       reinterpret_cast<unsigned long long *>(f->counters + 2), order,
+                           &f->params->order_on, st);
     mark(5);
     launches += 1;
     f->launches = launches;
@@ -216,16 +221,22 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
 }  // namespace
 
 namespace {
-// Render order of an image's 8x4 ray tiles. Two candidates: row-major
-// (nullptr) and centre-out (by distance of the tile centre from the image
-// centre, ties row-major), which starts a framed character's expensive
-// middle first so the cheap border fills the tail. Which one is faster
-// depends on the asset and view (measured: configs[2] 1.78 -> 1.72 ms and
-// configs[1] 2.26 -> 2.19 ms with centre-out, configs[4] 9.5 -> 10.9 ms),
-// so the first frame of each image size times both (calibrate_order) and
-// keeps the faster. Any order gives the same maps bit for bit: each ray is
-// independent and its own sums keep hit order. Cached per image size next
-// to the graphs that capture the choice.
+// Render order of an image's 8x4 ray tiles: row-major, or centre-out (by
+// distance of the tile centre from the image centre, ties row-major), which
+// starts a framed character's expensive middle first so the cheap border
+// fills the tail. Measured (same box, graph replay, L2 flushed): centre-out
+// takes configs[2]/[3] 1.78 -> 1.72 ms and configs[1] 2.25 -> 2.19 ms, but
+// configs[4] -- a 4.6 GB FLUT over 2.3 M-pixel eyes, whose in-flight rows
+// already overflow L2 (DRAM reads 2x the rows touched) -- 9.5 -> 10.9 ms:
+// a ring-shaped front of in-flight tiles re-reads more rows than a band.
+// So centre-out is used while the FLUT coefficients fit in 16x L2 (1.1 GB
+// at configs[2], 4.6 GB at configs[4]; ARTEMIS_TILE_ORDER=rowmajor|centre
+// overrides, artemis_frame_set_tile_order installs any permutation).
+// Per-frame trials of both orders were tried and rejected: frame-to-frame
+// and view-to-view variation swamps a 3 % difference. Any order gives the
+// same maps bit for bit: each ray is independent and its own sums keep hit
+// order. Cached per image size next to the graphs that capture it; the
+// choice travels in the parameter block, so one graph serves both.
 artemis_frame_s::OrderSlot *order_slot(artemis_frame f, int w, int h, int *rc) {
     *rc = ARTEMIS_OK;
     artemis_frame_s::OrderSlot *slot = nullptr, *victim = &f->orders[0];
@@ -268,7 +279,11 @@ artemis_frame_s::OrderSlot *order_slot(artemis_frame f, int w, int h, int *rc) {
         }
         slot->w = w;
         slot->h = h;
-        slot->mode = -1;
+        int l2 = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        const double flut = (double)f->n * (f->asset.degree + 1) * (f->asset.degree + 1) * f->asset.channels * 4.0;
+        slot->mode = flut <= 16.0 * (l2 > 0 ? l2 : (126 << 20)) ? 1 : 0;
         const char *e = getenv("ARTEMIS_TILE_ORDER");  // "rowmajor" / "centre" force one
         if (e && !strcmp(e, "rowmajor")) slot->mode = 0;
         if (e && !strcmp(e, "centre")) slot->mode = 1;
@@ -387,6 +402,7 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     if (f->staging) cudaFreeHost(f->staging);
     for (auto &o : f->orders)
         if (o.dev) cudaFree(o.dev);
+
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
                     f->leaves, f->btable, f->brecs, f->bmeta,
@@ -396,6 +412,10 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     delete f;
     return ARTEMIS_OK;
 }
+
+static int run_frame_launch(artemis_frame f, int identity, int n_joints, const artemis_camera *cam,
+                            int sharded, double lambda_th, double sigma_dep, int flags, float *F,
+                            void *alpha, void *depth, const int32_t *order, cudaStream_t st);
 
 extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const double *rot_inv,
                                  int n_joints, const artemis_camera *cam, double lambda_th,
@@ -429,39 +449,27 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
         ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, hp->rot_inv,
                                     sizeof(double) * 9 * n_joints, cudaMemcpyHostToDevice, st));
     }
-    ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));
     const int sharded = cam->tile_stride > 1;
     const int32_t *order = nullptr;
+    hp->order_on = 0;
     if (!sharded) {
         int rc = ARTEMIS_OK;
-        artemis_frame_s::OrderSlot *slot = order_slot(f, cam->width, cam->height, &rc);
-        if (!slot) return rc;
-        if (slot->mode < 0) {
-            // first frame of this size: time this frame's full pipeline with
-            // each order (eager, twice each, best of two) and keep the faster
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
-            ARTEMIS_TRY(cudaEventCreate(&e0));
-            ARTEMIS_TRY(cudaEventCreate(&e1));
-            float best[2] = {1e30f, 1e30f};
-            for (int rep = 0; rep < 2 && !rc; ++rep)
-                for (int m = 0; m < 2 && !rc; ++m) {
-                    cudaEventRecord(e0, st);
-                    rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, 0,
-                                       lambda_th, sigma_dep, flags & ~2, F, alpha, depth,
-                                       m ? slot->dev : nullptr, st);
-                    cudaEventRecord(e1, st);
-                    float ms = 0.0f;
-                    if (!rc && cudaEventSynchronize(e1) == cudaSuccess &&
-                        cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < best[m])
-                        best[m] = ms;
-                }
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-            if (rc) return rc;
-            slot->mode = best[1] < best[0] ? 1 : 0;
-        }
-        order = slot->mode ? slot->dev : nullptr;
+        artemis_frame_s::OrderSlot *oslot = order_slot(f, cam->width, cam->height, &rc);
+        if (!oslot) return rc;
+        order = oslot->dev;
+        hp->order_on = oslot->mode;
     }
+    ARTEMIS_TRY(cudaMemcpyAsync(&f->params->order_on, &hp->order_on, sizeof(int32_t),
+                                cudaMemcpyHostToDevice, st));
+    ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));  // the staging block may be reused after this
+    return run_frame_launch(f, identity, n_joints, cam, sharded, lambda_th, sigma_dep, flags, F,
+                            alpha, depth, order, st);
+}
+
+// Eager enqueue or graph capture / replay of one frame (artemis_frame_run).
+static int run_frame_launch(artemis_frame f, int identity, int n_joints, const artemis_camera *cam,
+                            int sharded, double lambda_th, double sigma_dep, int flags, float *F,
+                            void *alpha, void *depth, const int32_t *order, cudaStream_t st) {
     const int use_graph = (flags & 2) && st != nullptr;
     if (!use_graph)
         return enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded, lambda_th,

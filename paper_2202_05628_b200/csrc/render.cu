@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         tstride = p.cam->tile_stride;
     }
     const int64_t n_tiles = (int64_t)p.tiles_x * p.tiles_y;
-    const int32_t *order = kCamera ? p.tile_order : nullptr;
+    const int32_t *order =
+        kCamera && p.tile_order && (!p.order_on || __ldg(p.order_on)) ? p.tile_order : nullptr;
     const int64_t n_ids = kCamera ? (tstart < n_tiles ? (n_tiles - tstart + tstride - 1) / tstride : 0) * 32
                                   : p.n_rays;
     const unsigned lt = lanemask_lt();
@@ -969,9 +970,10 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
-                  cudaStream_t st) {
+                  const int32_t *order_on, cudaStream_t st) {
     RenderArgs a{};
     a.tile_order = sharded ? nullptr : tile_order;
+    a.order_on = order_on;
     fill_tree(a, tree);
     fill_shade(a, shade);
     a.cam = cam_dev;

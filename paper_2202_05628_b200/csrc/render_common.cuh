@@ -34,6 +34,7 @@ struct RenderArgs {
     int tiles_x, tiles_y;  // camera mode: ceil(W / 8), ceil(H / 4)
     unsigned long long *queue;  // ray-id counter, zero at launch
     const int32_t *tile_order;  // camera mode, unsharded: the i-th 8x4 tile to visit (a permutation)
+    const int32_t *order_on;    // device flag: use tile_order (else row-major); null = use it
     double t_min, t_max;
     double stop;  // 1 - lambda_th
     float coord_max;  // upper bound of every box coordinate (grid resolution)
