@@ -58,9 +58,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=2)
-    ap.add_argument("--shard", default="frames", choices=["frames", "tiles"],
-                    help="N>1: frames (weak scaling, no collective) or 8x4 screen tiles of "
-                         "the same frame (strong scaling, one NCCL gather per frame)")
+    ap.add_argument("--shard", default="frames", choices=["frames", "tiles", "peer"],
+                    help="N>1: frames (weak scaling, no collective), 8x4 screen tiles of "
+                         "the same frame (strong scaling, one NCCL gather per frame), or "
+                         "tiles stored by the render kernels straight into rank 0's maps "
+                         "over NVLink (peer: CUDA IPC mapping, no gather)")
     return ap.parse_args()
 
 
@@ -236,7 +238,8 @@ def main():
     n_frames = args.warmup + args.steps
     sc = make_scene(args.config, max(64, n_frames * world) if args.config == "c2" else n_frames)
     frames = [(rank + world * s) % len(sc.poses) for s in range(n_frames)]
-    tiles = args.shard == "tiles" and world > 1
+    tiles = args.shard in ("tiles", "peer") and world > 1
+    peer = args.shard == "peer" and world > 1
     if tiles:  # every rank renders the same frame sequence, its own tiles
         frames = [s % len(sc.poses) for s in range(n_frames)]
         from paper_2202_05628_b200 import parallel as PL
@@ -247,8 +250,12 @@ def main():
     rays = W * H
     stream = fp.stream
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    asm = PL.PeerAssembly(fp, W, H) if peer else None
 
     def frame(f, graph=True):
+        if peer:
+            return asm.frame(KM.PoseSpec.make(sc.poses[f]), cams[f], lambda_th=sc.lambda_th,
+                             sigma_dep=sc.sigma_dep, graph=graph, tables=tables[f])
         out = fp.run(KM.PoseSpec.make(sc.poses[f]), cams[f],
                      lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep, graph=graph,
                      tables=tables[f], tiles=(rank, world) if tiles else None)
@@ -373,7 +380,10 @@ def main():
                        "voxels": sc.n_voxels, "live_leaves": n_live, "in_bounds": n_in,
                        "channels": sc.channels, "sh_degree": sc.degree,
                        "frames_per_rank": args.steps,
-                       "parallelism": (f"tiles-sharded x{world} (8x4 tiles t % {world}, one "
+                       "parallelism": (f"tiles-sharded x{world} (8x4 tiles t % {world}, "
+                                       f"stored into rank 0's maps by the render kernels over "
+                                       f"NVLink)" if peer else
+                                       f"tiles-sharded x{world} (8x4 tiles t % {world}, one "
                                        f"NCCL gather per frame)" if tiles
                                        else f"frames-sharded x{world}"),
                        "l2": "flushed between timed frames (256 MB write)",

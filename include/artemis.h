@@ -331,6 +331,16 @@ int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double
                       double sigma_dep, int flags, float *F, void *alpha, void *depth,
                       artemis_stream stream);
 
+/* Tile-sharded frames (camera tile_stride > 1) of this handle write their
+ * pixels straight into F / alpha / depth -- the destination rank's
+ * full-frame buffers mapped into this process (CUDA IPC, peer access over
+ * NVLink), or this rank's own on the destination -- instead of the local
+ * outputs (left untouched). The destination initialises them (F 0, alpha 0,
+ * depth +inf) before any rank renders; each rank writes exactly its own
+ * tiles, so the assembled frame needs no gather. alpha/depth are float, or
+ * double with ARTEMIS_FRAME_MAPS64. F == NULL restores the local outputs. */
+int artemis_frame_set_output_peer(artemis_frame frame, float *F, void *alpha, void *depth);
+
 /* Render order of the 8x4 ray tiles for one image size: `order` (HOST,
  * ceil(w/8)*ceil(h/4) int32) must be a permutation of the tile indices
  * (row-major tile numbering); ARTEMIS_ERR_ARG otherwise. Without it the

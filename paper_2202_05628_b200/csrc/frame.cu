@@ -36,7 +36,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
-                  const int32_t *order_on, cudaStream_t st);
+                  const int32_t *order_on, void *const *peer_out, cudaStream_t st);
 
 constexpr int kMaxFrameJoints = 256;
 
@@ -106,6 +106,9 @@ struct artemis_frame_s {
     // stage profiling (eager runs only): events before warp, sort, resolve,
     // build, render and after render
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    // tile-sharded frames written straight into another rank's full-frame
+    // F / alpha / depth (peer memory over NVLink): artemis_frame_set_output_peer
+    void *peer_out[3] = {nullptr, nullptr, nullptr};
     int profile = 0;
 };
 
@@ -142,7 +145,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th,
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
-                           &f->params->order_on, st);
+                           &f->params->order_on, sharded ? f->peer_out : nullptr, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -211,7 +214,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
                        flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                        reinterpret_cast<unsigned long long *>(f->counters + 2), order,
-                           &f->params->order_on, st);
+                           &f->params->order_on, sharded ? f->peer_out : nullptr, st);
     mark(5);
     launches += 1;
     f->launches = launches;
@@ -292,6 +295,26 @@ artemis_frame_s::OrderSlot *order_slot(artemis_frame f, int w, int h, int *rc) {
     return slot;
 }
 }  // namespace
+
+// Tile-sharded frames of this handle write their pixels into (F, alpha,
+// depth) -- another rank's full-frame buffers mapped into this process
+// (CUDA IPC; peer access over NVLink) or this rank's own -- instead of the
+// local outputs, which then stay untouched. The owner initialises the maps
+// (F 0, alpha 0, depth +inf) before any rank renders; every rank writes only
+// its own tiles, so the assembled frame needs no gather. NULLs restore the
+// local outputs. Captured graphs are dropped (they bake the pointers).
+extern "C" int artemis_frame_set_output_peer(artemis_frame f, float *F, void *alpha, void *depth) {
+    if (!f || (F && (!alpha || !depth))) return ARTEMIS_ERR_ARG;
+    for (auto &g : f->graphs)
+        if (g.exec) {
+            cudaGraphExecDestroy(g.exec);
+            g.exec = nullptr;
+        }
+    f->peer_out[0] = F;
+    f->peer_out[1] = F ? alpha : nullptr;
+    f->peer_out[2] = F ? depth : nullptr;
+    return ARTEMIS_OK;
+}
 
 // Install a caller-supplied render order (a permutation of the w x h image's
 // 8x4 tiles, host array) for that image size; graphs captured for the size

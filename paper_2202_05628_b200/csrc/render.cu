@@ -970,7 +970,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
-                  const int32_t *order_on, cudaStream_t st) {
+                  const int32_t *order_on, void *const *peer_out, cudaStream_t st) {
     RenderArgs a{};
     a.tile_order = sharded ? nullptr : tile_order;
     a.order_on = order_on;
@@ -979,8 +979,16 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
     a.cam = cam_dev;
     a.queue = queue;
     const int64_t n = (int64_t)width * height;
-    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * shade->channels * sizeof(float), st));
-    if (sharded) {  // pixels of other ranks' tiles: alpha 0, depth +inf
+    // peer outputs: another rank's full-frame buffers (initialised by their
+    // owner); this launch writes exactly its own tiles' pixels into them
+    const bool peer = peer_out && peer_out[0];
+    if (peer) {
+        F = static_cast<float *>(peer_out[0]);
+        A = peer_out[1];
+        D = peer_out[2];
+    }
+    if (!peer) ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * shade->channels * sizeof(float), st));
+    if (sharded && !peer) {  // pixels of other ranks' tiles: alpha 0, depth +inf
         const int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148);
         if (maps64)
             fill_alpha_depth<double><<<g, 256, 0, st>>>(static_cast<double *>(A),

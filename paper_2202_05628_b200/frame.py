@@ -439,6 +439,14 @@ class FramePipeline:
         out["root"] = 0 if n_live > 1 else ~0
         return out
 
+    def set_output_peer(self, F=None, alpha=None, depth=None) -> None:
+        """Tile-sharded frames write their pixels into these full-frame device
+        tensors (the destination rank's, mapped over CUDA IPC / NVLink)
+        instead of this pipeline's outputs; None restores the local ones."""
+        check(_lib.lib().artemis_frame_set_output_peer(
+            self._h, ptr(F) if F is not None else None, ptr(alpha) if F is not None else None,
+            ptr(depth) if F is not None else None), "frame_set_output_peer")
+
     def set_tile_order(self, width: int, height: int, order) -> None:
         """Render the 8x4 ray tiles of a width x height image in `order` (a
         permutation of the row-major tile indices); the maps do not change."""

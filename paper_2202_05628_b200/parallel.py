@@ -13,7 +13,11 @@ shards without any exchange inside a frame:
           gather moves the shards to the root, and the root unpacks them
           into the image (artemis_tiles_unpack). Only rendered pixels cross
           NVLink ((world-1)/world of the frame), and the assembled frame is
-          bit-identical to a single-GPU render.
+          bit-identical to a single-GPU render;
+          or, with PeerAssembly, no gather at all: every rank's render
+          kernel writes its tiles' pixels straight into the root's
+          full-frame buffers (CUDA IPC mapping, peer stores over NVLink),
+          overlapping the transfer with the render ray by ray.
 """
 
 from __future__ import annotations
@@ -126,3 +130,59 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+class PeerAssembly:
+    """Tile-sharded frames assembled by the render kernels themselves.
+
+    The root (`dst`) owns full-frame F / alpha / depth device tensors; every
+    other rank maps them into its address space (CUDA IPC handles, exchanged
+    once through torch.distributed) and hands them to its FramePipeline
+    (artemis_frame_set_output_peer). A frame is then: root initialises the
+    maps -> barrier -> every rank renders its tiles (t % world == rank),
+    its kernel storing each finished ray's pixels directly into the root's
+    maps over NVLink -> stream sync + barrier -> the root holds the whole
+    image. No pack, no collective on the data path, no unpack; bit-identical
+    to a single-GPU render (every pixel is written by exactly one rank)."""
+
+    def __init__(self, fp, width: int, height: int, *, maps64: bool = False, dst: int = 0):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.fp, self.width, self.height, self.dst = fp, int(width), int(height), dst
+        self.rank, self.world = world()
+        n = self.width * self.height
+        mt = torch.float64 if maps64 else torch.float32
+        self.maps64 = maps64
+        if self.rank == dst:
+            self.F = torch.zeros((n, fp.channels), dtype=torch.float32, device="cuda")
+            self.A = torch.zeros(n, dtype=mt, device="cuda")
+            self.D = torch.full((n,), float("inf"), dtype=mt, device="cuda")
+            shared = [[reduce_tensor(t) for t in (self.F, self.A, self.D)]]
+        else:
+            shared = [None]
+        if self.world > 1:
+            dist.broadcast_object_list(shared, src=dst)
+        if self.rank != dst:
+            self.F, self.A, self.D = (fn(*args) for fn, args in shared[0])
+        fp.set_output_peer(self.F, self.A, self.D)
+
+    def frame(self, pose, camera, **kw):
+        """Render one tile-sharded frame into the root's maps; returns the
+        root's (F, alpha, depth) on the root, None elsewhere."""
+        if self.rank == self.dst:
+            with torch.cuda.stream(self.fp.stream):
+                self.F.zero_()
+                self.A.zero_()
+                self.D.fill_(float("inf"))
+        self.fp.stream.synchronize()
+        if self.world > 1:
+            dist.barrier()  # the root's maps are initialised before any rank stores
+        self.fp.run(pose, camera, tiles=tile_shard(self.rank, self.world), maps64=self.maps64,
+                    **kw)
+        self.fp.stream.synchronize()
+        if self.world > 1:
+            dist.barrier()  # every rank's stores have landed
+        return (self.F, self.A, self.D) if self.rank == self.dst else None
+
+    def close(self):
+        self.fp.set_output_peer(None)
