@@ -350,6 +350,17 @@ int artemis_frame_set_output_peer(artemis_frame frame, float *F, void *alpha, vo
 int artemis_frame_set_tile_order(artemis_frame frame, int width, int height,
                                  const int32_t *order);
 
+/* One pose, several views (configs[1] views, configs[4] stereo eyes): warp
+ * + rebuild once, then ONE render launch over all n_views (<= 8) cameras of
+ * the same image size, their 8x4 tiles interleaved in the ray queue so the
+ * views' rays over the same leaves are in flight together and share the
+ * FLUT rows in L2. Outputs per view: F[v], alpha[v], depth[v] (as
+ * artemis_frame_run). Unsharded cameras only. Flags as artemis_frame_run. */
+int artemis_frame_run_views(artemis_frame frame, const double *joint_aff, const double *rot_inv,
+                            int n_joints, const artemis_camera *cams, int n_views,
+                            double lambda_th, double sigma_dep, int flags, float *const *F,
+                            void *const *alpha, void *const *depth, artemis_stream stream);
+
 /* Read back the last frame's counts (synchronises the stream). */
 int artemis_frame_counts(artemis_frame frame, int64_t *n_in_bounds, int64_t *n_live,
                          artemis_stream stream);

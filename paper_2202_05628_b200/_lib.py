@@ -108,6 +108,7 @@ _SIGS = {
     "artemis_frame_launches": (INT, [P]),
     "artemis_frame_set_tile_order": (INT, [P, INT, INT, P]),
     "artemis_frame_set_output_peer": (INT, [P, P, P, P]),
+    "artemis_frame_run_views": (INT, [P, P, P, INT, P, INT, DBL, DBL, INT, P, P, P, P]),
     "artemis_copy_to_host": (INT, [P, P, SZ, P]),
     "artemis_frame_profile": (INT, [P, INT]),
     "artemis_brickmap_bytes": (SZ, [I64, P]),

@@ -23,6 +23,7 @@
 
 #include "bricks.cuh"
 #include "common.cuh"
+#include "render_common.cuh"
 #include "tree.cuh"
 
 namespace artemis {
@@ -36,12 +37,21 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
-                  const int32_t *order_on, void *const *peer_out, cudaStream_t st);
+                  const int32_t *order_on, void *const *peer_out, int n_views,
+                  float *const *Fv, void *const *Av, void *const *Dv, cudaStream_t st);
+
+// per-view outputs of a multi-view frame (artemis_frame_run_views)
+struct ViewOut {
+    int n = 1;
+    float *F[kMaxViews] = {};
+    void *A[kMaxViews] = {};
+    void *D[kMaxViews] = {};
+};
 
 constexpr int kMaxFrameJoints = 256;
 
 struct FrameParams {
-    artemis_camera cam;
+    artemis_camera cam[kMaxViews];  // the frame's views (one unless artemis_frame_run_views)
     int32_t order_on;  // render the ray tiles in the size's centre-out order (else row-major)
     int32_t pad;
     double aff[kMaxFrameJoints * 12];
@@ -87,6 +97,7 @@ struct artemis_frame_s {
         const void *F = nullptr, *A = nullptr, *D = nullptr;
         cudaStream_t stream = nullptr;
         double lambda = 0, sigma_dep = 0;
+        ViewOut views;
         unsigned long long used = 0;
     };
     static constexpr int kGraphSlots = 4;
@@ -106,6 +117,10 @@ struct artemis_frame_s {
     // stage profiling (eager runs only): events before warp, sort, resolve,
     // build, render and after render
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    // FLUT coefficients within 16x L2: centre-out tile order, several views
+    // per render launch (order_slot, enqueue_frame); row-major and one launch
+    // per view beyond
+    int small_flut = 1;
     // tile-sharded frames written straight into another rank's full-frame
     // F / alpha / depth (peer memory over NVLink): artemis_frame_set_output_peer
     void *peer_out[3] = {nullptr, nullptr, nullptr};
@@ -126,7 +141,7 @@ int dev_alloc(T **p, size_t bytes) {
 
 int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int height,
                   int sharded, double lambda_th, double sigma_dep, int flags, float *F, void *A,
-                  void *D, const int32_t *order, cudaStream_t st) {
+                  void *D, const int32_t *order, const ViewOut &vo, cudaStream_t st) {
     const artemis_asset &as = f->asset;
     int rc;
     int launches = 0;
@@ -142,10 +157,11 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                              &f->bmap};
         artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                            as.channels, 0};
-        rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th,
+        rc = render_camera(&tv, &sh, f->params->cam, width, height, sharded, lambda_th,
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
-                           &f->params->order_on, sharded ? f->peer_out : nullptr, st);
+                           &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
+                           vo.D, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -211,10 +227,25 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution, &f->bmap};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
-    rc = render_camera(&tv, &sh, &f->params->cam, width, height, sharded, lambda_th, sigma_dep,
-                       flags & 1, (flags & 8) ? 1 : 0, F, A, D,
-                       reinterpret_cast<unsigned long long *>(f->counters + 2), order,
-                           &f->params->order_on, sharded ? f->peer_out : nullptr, st);
+    if (vo.n > 1 && !f->small_flut) {
+        // big FLUT: the views' rows would not stay in L2 together (configs[4]
+        // stereo: one launch 10.4 ms vs 9.6 ms for two), so one launch per view
+        for (int v = 0; v < vo.n && !rc; ++v) {
+            if (v) ARTEMIS_TRY(cudaMemsetAsync(f->counters + 2, 0, 2 * sizeof(int32_t), st));
+            rc = render_camera(&tv, &sh, f->params->cam + v, width, height, 0, lambda_th,
+                               sigma_dep, flags & 1, (flags & 8) ? 1 : 0, vo.F[v], vo.A[v],
+                               vo.D[v], reinterpret_cast<unsigned long long *>(f->counters + 2),
+                               order, &f->params->order_on, nullptr, 1, nullptr, nullptr, nullptr,
+                               st);
+        }
+        launches += vo.n - 1;
+    } else {
+        rc = render_camera(&tv, &sh, f->params->cam, width, height, sharded, lambda_th, sigma_dep,
+                           flags & 1, (flags & 8) ? 1 : 0, F, A, D,
+                           reinterpret_cast<unsigned long long *>(f->counters + 2), order,
+                           &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
+                           vo.D, st);
+    }
     mark(5);
     launches += 1;
     f->launches = launches;
@@ -224,6 +255,13 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
 }  // namespace
 
 namespace {
+bool same_views(const ViewOut &a, const ViewOut &b) {
+    if (a.n != b.n) return false;
+    for (int v = 0; v < a.n && a.n > 1; ++v)
+        if (a.F[v] != b.F[v] || a.A[v] != b.A[v] || a.D[v] != b.D[v]) return false;
+    return true;
+}
+
 // Render order of an image's 8x4 ray tiles: row-major, or centre-out (by
 // distance of the tile centre from the image centre, ties row-major), which
 // starts a framed character's expensive middle first so the cheap border
@@ -282,11 +320,7 @@ artemis_frame_s::OrderSlot *order_slot(artemis_frame f, int w, int h, int *rc) {
         }
         slot->w = w;
         slot->h = h;
-        int l2 = 0, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        const double flut = (double)f->n * (f->asset.degree + 1) * (f->asset.degree + 1) * f->asset.channels * 4.0;
-        slot->mode = flut <= 16.0 * (l2 > 0 ? l2 : (126 << 20)) ? 1 : 0;
+        slot->mode = f->small_flut ? 1 : 0;
         const char *e = getenv("ARTEMIS_TILE_ORDER");  // "rowmajor" / "centre" force one
         if (e && !strcmp(e, "rowmajor")) slot->mode = 0;
         if (e && !strcmp(e, "centre")) slot->mode = 1;
@@ -363,6 +397,13 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     }
     const int64_t n = f->n;
     int rc = ARTEMIS_OK;
+    {
+        int l2 = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        const double flut = (double)n * (a->degree + 1) * (a->degree + 1) * a->channels * 4.0;
+        f->small_flut = flut <= 16.0 * (l2 > 0 ? l2 : (126 << 20));
+    }
     rc = rc ? rc : dev_alloc(&f->keys, n * f->key_bytes);
     rc = rc ? rc : dev_alloc(&f->keys_sorted, n * f->key_bytes);
     rc = rc ? rc : dev_alloc(&f->live_codes, n * f->key_bytes);
@@ -438,14 +479,23 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
 
 static int run_frame_launch(artemis_frame f, int identity, int n_joints, const artemis_camera *cam,
                             int sharded, double lambda_th, double sigma_dep, int flags, float *F,
-                            void *alpha, void *depth, const int32_t *order, cudaStream_t st);
+                            void *alpha, void *depth, const int32_t *order, const ViewOut &vo,
+                            cudaStream_t st);
 
-extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const double *rot_inv,
-                                 int n_joints, const artemis_camera *cam, double lambda_th,
-                                 double sigma_dep, int flags, float *F, void *alpha,
-                                 void *depth, artemis_stream stream) {
-    if (!f || !cam || !F || !alpha || !depth || cam->width < 1 || cam->height < 1)
+// One posed frame: warp + rebuild once, then one render launch over the
+// views cam[0 .. vo.n) (the outputs of view v in vo, or F/alpha/depth for a
+// single view).
+static int frame_run_impl(artemis_frame f, const double *joint_aff, const double *rot_inv,
+                          int n_joints, const artemis_camera *cam, double lambda_th,
+                          double sigma_dep, int flags, float *F, void *alpha, void *depth,
+                          const ViewOut &vo, artemis_stream stream) {
+    if (!f || !cam || !F || !alpha || !depth || cam->width < 1 || cam->height < 1 || vo.n < 1 ||
+        vo.n > kMaxViews)
         return ARTEMIS_ERR_ARG;
+    for (int v = 1; v < vo.n; ++v)
+        if (cam[v].width != cam->width || cam[v].height != cam->height || cam[v].tile_stride > 1)
+            return ARTEMIS_ERR_ARG;
+    if (vo.n > 1 && cam->tile_stride > 1) return ARTEMIS_ERR_ARG;
     const int identity = joint_aff == nullptr;
     if (!identity && (!rot_inv || n_joints < 1 || n_joints > f->asset.max_joints))
         return ARTEMIS_ERR_ARG;
@@ -456,8 +506,8 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
     f->stage_next = (sidx + 1) % artemis_frame_s::kStaging;
     FrameParams *hp = f->staging + sidx;
     ARTEMIS_TRY(cudaEventSynchronize(f->staged[sidx]));  // its last copy has completed
-    hp->cam = *cam;
-    ARTEMIS_TRY(cudaMemcpyAsync(&f->params->cam, &hp->cam, sizeof(artemis_camera),
+    for (int v = 0; v < vo.n; ++v) hp->cam[v] = cam[v];
+    ARTEMIS_TRY(cudaMemcpyAsync(f->params->cam, hp->cam, sizeof(artemis_camera) * vo.n,
                                 cudaMemcpyHostToDevice, st));
     if (identity) {
         static const double eye[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
@@ -486,23 +536,52 @@ extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const
                                 cudaMemcpyHostToDevice, st));
     ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));  // the staging block may be reused after this
     return run_frame_launch(f, identity, n_joints, cam, sharded, lambda_th, sigma_dep, flags, F,
-                            alpha, depth, order, st);
+                            alpha, depth, order, vo, st);
+}
+
+extern "C" int artemis_frame_run(artemis_frame f, const double *joint_aff, const double *rot_inv,
+                                 int n_joints, const artemis_camera *cam, double lambda_th,
+                                 double sigma_dep, int flags, float *F, void *alpha,
+                                 void *depth, artemis_stream stream) {
+    ViewOut vo;
+    return frame_run_impl(f, joint_aff, rot_inv, n_joints, cam, lambda_th, sigma_dep, flags, F,
+                          alpha, depth, vo, stream);
+}
+
+extern "C" int artemis_frame_run_views(artemis_frame f, const double *joint_aff,
+                                       const double *rot_inv, int n_joints,
+                                       const artemis_camera *cams, int n_views, double lambda_th,
+                                       double sigma_dep, int flags, float *const *F,
+                                       void *const *alpha, void *const *depth,
+                                       artemis_stream stream) {
+    if (n_views < 1 || n_views > kMaxViews || !F || !alpha || !depth) return ARTEMIS_ERR_ARG;
+    ViewOut vo;
+    vo.n = n_views;
+    for (int v = 0; v < n_views; ++v) {
+        if (!F[v] || !alpha[v] || !depth[v]) return ARTEMIS_ERR_ARG;
+        vo.F[v] = F[v];
+        vo.A[v] = alpha[v];
+        vo.D[v] = depth[v];
+    }
+    return frame_run_impl(f, joint_aff, rot_inv, n_joints, cams, lambda_th, sigma_dep, flags,
+                          F[0], alpha[0], depth[0], vo, stream);
 }
 
 // Eager enqueue or graph capture / replay of one frame (artemis_frame_run).
 static int run_frame_launch(artemis_frame f, int identity, int n_joints, const artemis_camera *cam,
                             int sharded, double lambda_th, double sigma_dep, int flags, float *F,
-                            void *alpha, void *depth, const int32_t *order, cudaStream_t st) {
+                            void *alpha, void *depth, const int32_t *order, const ViewOut &vo,
+                            cudaStream_t st) {
     const int use_graph = (flags & 2) && st != nullptr;
     if (!use_graph)
         return enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded, lambda_th,
-                             sigma_dep, flags, F, alpha, depth, order, st);
+                             sigma_dep, flags, F, alpha, depth, order, vo, st);
     artemis_frame_s::GraphSlot *slot = nullptr, *victim = &f->graphs[0];
     for (auto &g : f->graphs) {
         if (g.exec && g.w == cam->width && g.h == cam->height && g.flags == flags &&
             g.identity == identity && g.nj == n_joints && g.F == F && g.A == alpha &&
             g.D == depth && g.stream == st && g.lambda == lambda_th &&
-            g.sigma_dep == sigma_dep && g.sharded == sharded) {
+            g.sigma_dep == sigma_dep && g.sharded == sharded && same_views(g.views, vo)) {
             slot = &g;
             break;
         }
@@ -516,7 +595,7 @@ static int run_frame_launch(artemis_frame f, int identity, int n_joints, const a
         }
         ARTEMIS_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         int rc = enqueue_frame(f, identity, n_joints, cam->width, cam->height, sharded,
-                               lambda_th, sigma_dep, flags, F, alpha, depth, order, st);
+                               lambda_th, sigma_dep, flags, F, alpha, depth, order, vo, st);
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(st, &g);
         if (rc) {
@@ -546,6 +625,7 @@ static int run_frame_launch(artemis_frame f, int identity, int n_joints, const a
         slot->lambda = lambda_th;
         slot->sigma_dep = sigma_dep;
         slot->sharded = sharded;
+        slot->views = vo;
     }
     slot->used = ++f->graph_clock;
     ARTEMIS_TRY(cudaGraphLaunch(slot->exec, st));

@@ -253,7 +253,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     const int64_t n_tiles = (int64_t)p.tiles_x * p.tiles_y;
     const int32_t *order =
         kCamera && p.tile_order && (!p.order_on || __ldg(p.order_on)) ? p.tile_order : nullptr;
-    const int64_t n_ids = kCamera ? (tstart < n_tiles ? (n_tiles - tstart + tstride - 1) / tstride : 0) * 32
+    // camera mode: the tiles of all views interleave in the ray queue (tile t
+    // of view 0, of view 1, ..., then tile t + 1), so the views' rays over
+    // the same leaves are in flight together and share their FLUT rows in L2
+    const int nv = kCamera && p.n_views > 1 ? p.n_views : 1;
+    const int64_t n_ids = kCamera ? (tstart < n_tiles ? (n_tiles - tstart + tstride - 1) / tstride : 0) * 32 * nv
                                   : p.n_rays;
     const unsigned lt = lanemask_lt();
     const int wbase = warp * 32;  // this warp's column block in the queue arrays
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // round (phase B2) and at retirement, so it lives in shared memory
     double *s_tad = s_dw + 3 * kRenderThreads + 3 * tid;
     int64_t hits = 0, trace_base = 0;
+    int rv = 0;  // camera mode: view of this lane's ray
     int cur = kEnd, top = 0, nq = 0;
     int ovf[kStack - kSmemStack];
     bool queue_open = true;
@@ -471,8 +476,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         ray = -1;
         double dw[3];
         if (kCamera) {
-            const artemis_camera &cam = *p.cam;
-            const int64_t t = tstart + (id >> 5) * tstride;
+            const int64_t gi = id >> 5;
+            rv = nv > 1 ? (int)(gi % nv) : 0;
+            const artemis_camera &cam = p.cam[rv];
+            const int64_t t = tstart + (nv > 1 ? gi / nv : gi) * tstride;
             const int64_t tile = order ? (int64_t)__ldg(order + t) : t;
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
@@ -844,11 +851,21 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             if (kMode == kCount) {
                 p.counts[ray] = hits;
             } else {
-                if (p.A64) p.A64[ray] = acc;
-                if (p.A32) p.A32[ray] = (float)acc;
-                if (kMode == kRender) {
-                    if (p.D64) p.D64[ray] = depth;
-                    if (p.D32) p.D32[ray] = (float)depth;
+                if (nv > 1) {  // per-view maps
+                    if (p.A64) {
+                        static_cast<double *>(p.Av[rv])[ray] = acc;
+                        static_cast<double *>(p.Dv[rv])[ray] = depth;
+                    } else {
+                        static_cast<float *>(p.Av[rv])[ray] = (float)acc;
+                        static_cast<float *>(p.Dv[rv])[ray] = (float)depth;
+                    }
+                } else {
+                    if (p.A64) p.A64[ray] = acc;
+                    if (p.A32) p.A32[ray] = (float)acc;
+                    if (kMode == kRender) {
+                        if (p.D64) p.D64[ray] = depth;
+                        if (p.D32) p.D32[ray] = (float)depth;
+                    }
                 }
             }
         }
@@ -859,8 +876,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const int s = __ffs(fm) - 1;
                 fm &= fm - 1;
                 const int64_t r = __shfl_sync(0xffffffffu, ray, s);
+                float *Fo = p.F;
+                if (kCamera && nv > 1) Fo = p.Fv[__shfl_sync(0xffffffffu, rv, s)];
                 for (int c = lane; c < C; c += 32) {
-                    p.F[r * C + c] = feat[s * cp + c];
+                    Fo[r * C + c] = feat[s * cp + c];
                     feat[s * cp + c] = FeatT(0);
                 }
             }
@@ -970,8 +989,23 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
-                  const int32_t *order_on, void *const *peer_out, cudaStream_t st) {
+                  const int32_t *order_on, void *const *peer_out, int n_views,
+                  float *const *Fv, void *const *Av, void *const *Dv, cudaStream_t st) {
     RenderArgs a{};
+    if (n_views > 1) {  // several views of one tree in one launch (unsharded, own outputs)
+        if (n_views > kMaxViews || sharded || (peer_out && peer_out[0])) return ARTEMIS_ERR_ARG;
+        const int64_t n = (int64_t)width * height;
+        for (int v = 0; v < n_views; ++v) {
+            ARTEMIS_TRY(cudaMemsetAsync(Fv[v], 0, (size_t)n * shade->channels * sizeof(float), st));
+            a.Fv[v] = Fv[v];
+            a.Av[v] = Av[v];
+            a.Dv[v] = Dv[v];
+        }
+        a.n_views = n_views;
+        F = Fv[0];
+        A = Av[0];
+        D = Dv[0];
+    }
     a.tile_order = sharded ? nullptr : tile_order;
     a.order_on = order_on;
     fill_tree(a, tree);
@@ -987,7 +1021,8 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         A = peer_out[1];
         D = peer_out[2];
     }
-    if (!peer) ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * shade->channels * sizeof(float), st));
+    if (!peer && n_views <= 1)
+        ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * shade->channels * sizeof(float), st));
     if (sharded && !peer) {  // pixels of other ranks' tiles: alpha 0, depth +inf
         const int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148);
         if (maps64)
@@ -1013,7 +1048,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         a.A32 = static_cast<float *>(A);
         a.D32 = static_cast<float *>(D);
     }
-    const int64_t warps = (int64_t)a.tiles_x * ((height + 3) / 4);
+    const int64_t warps = (int64_t)a.tiles_x * ((height + 3) / 4) * (n_views > 1 ? n_views : 1);
     return maps64 ? launch_render_deg<kRender, 2>(shade->degree, a, warps, st)
                   : launch_render_deg<kRender, 1>(shade->degree, a, warps, st);
 }

@@ -10,6 +10,8 @@
 
 namespace artemis {
 
+constexpr int kMaxViews = 8;  // views one camera-mode launch renders together
+
 enum RenderMode { kRender = 0, kTrace = 1, kCount = 2 };
 
 constexpr uint32_t kDenseFlag = 1u << 31;  // queued row's density exceeds sigma_dep
@@ -35,6 +37,13 @@ struct RenderArgs {
     unsigned long long *queue;  // ray-id counter, zero at launch
     const int32_t *tile_order;  // camera mode, unsharded: the i-th 8x4 tile to visit (a permutation)
     const int32_t *order_on;    // device flag: use tile_order (else row-major); null = use it
+    // camera mode: views rendered by this launch (cam[0 .. n_views), one
+    // image size); with n_views > 1 the outputs of view v are Fv/Av/Dv[v]
+    // (alpha/depth float, or double with A64/D64 set non-null)
+    int n_views;
+    float *Fv[kMaxViews];
+    void *Av[kMaxViews];
+    void *Dv[kMaxViews];
     double t_min, t_max;
     double stop;  // 1 - lambda_th
     float coord_max;  // upper bound of every box coordinate (grid resolution)

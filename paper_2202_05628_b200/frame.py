@@ -164,15 +164,74 @@ class FramePipeline:
             cur.wait_stream(self.stream)  # consumers on the caller's stream see the frame
         return F, A, D
 
+    def view_outputs(self, width: int, height: int, n: int, maps64: bool = False):
+        """Persistent per-view device outputs for run_views."""
+        key = ("views", width, height, n, bool(maps64))
+        if key not in self._outs:
+            with torch.cuda.stream(self.stream):
+                mt = np.float64 if maps64 else np.float32
+                px = width * height
+                self._outs[key] = [(empty((px, self.channels), np.float32), empty(px, mt),
+                                    empty(px, mt)) for _ in range(n)]
+        return self._outs[key]
+
+    def run_views(self, pose, cameras, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
+                  early_stop: bool = True, graph: bool = True, tables=None,
+                  maps64: bool = False, outs=None):
+        """One pose, up to 8 views of one image size (configs[1] views,
+        configs[4] stereo eyes): warp + rebuild once and ONE render launch
+        whose ray queue interleaves the views' 8x4 tiles, so rays of
+        different views over the same leaves share the FLUT rows in L2.
+        Returns the views' device (F, alpha, depth) (persistent buffers,
+        overwritten by the next call with the same shape)."""
+        L = _lib.lib()
+        cams = [c if isinstance(c, _lib.Camera) else self.camera(c) for c in cameras]
+        n = len(cams)
+        if not 1 <= n <= 8 or any((c.width, c.height) != (cams[0].width, cams[0].height)
+                                  for c in cams):
+            raise ValueError("run_views takes 1..8 cameras of one image size")
+        if pose is None or self.rig is None:
+            aff = rot = None
+            nj = 1
+        else:
+            t = tables if tables is not None else self.tables(pose)
+            aff = np.ascontiguousarray(t.affine34)
+            rot = np.ascontiguousarray(t.rot_inv.reshape(-1, 9))
+            nj = int(aff.shape[0])
+        outs = outs if outs is not None else self.view_outputs(cams[0].width, cams[0].height, n,
+                                                               maps64)
+        carr = (_lib.Camera * n)(*cams)
+        pa = (C.c_void_p * n)
+        Fs, As, Ds = (pa(*[ptr(o[k]) for o in outs]) for k in range(3))
+        flags = (1 if early_stop else 0) | (2 if graph else 0) | (8 if maps64 else 0)
+        check(L.artemis_frame_run_views(self._h, aff.ctypes.data if aff is not None else None,
+                                        rot.ctypes.data if rot is not None else None, nj,
+                                        C.cast(carr, C.c_void_p), n, float(lambda_th),
+                                        float(sigma_dep), flags, C.cast(Fs, C.c_void_p),
+                                        C.cast(As, C.c_void_p), C.cast(Ds, C.c_void_p),
+                                        self.stream.cuda_stream or None), "frame_run_views")
+        cur = torch.cuda.current_stream()
+        if cur != self.stream:
+            cur.wait_stream(self.stream)
+        return outs
+
     def render_views(self, pose, cameras, *, lambda_th: float = 1e-4, sigma_dep: float = 5.0,
                      early_stop: bool = True, graph: bool = True, tables=None):
         """One pose, several cameras (configs[1] views, configs[4] stereo
-        eyes): warp + rebuild once, then one render per camera. Returns a
-        list of device (F, alpha, depth) clones, one per camera."""
+        eyes): warp + rebuild once, then the views rendered together
+        (run_views; one render per camera when sizes differ or there are
+        more than 8). Returns a list of device (F, alpha, depth) clones."""
         t = tables if tables is not None or pose is None or self.rig is None \
             else self.tables(pose)
+        cams = [c if isinstance(c, _lib.Camera) else self.camera(c) for c in cameras]
+        if 1 <= len(cams) <= 8 and all((c.width, c.height) == (cams[0].width, cams[0].height)
+                                       for c in cams):
+            res = self.run_views(pose, cams, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                                 early_stop=early_stop, graph=graph, tables=t)
+            with torch.cuda.stream(self.stream):
+                return [tuple(x.clone() for x in o) for o in res]
         outs = []
-        for i, cam in enumerate(cameras):
+        for i, cam in enumerate(cams):
             F, A, D = self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
                                early_stop=early_stop, graph=graph, tables=t,
                                reuse_tree=i > 0)

@@ -39,8 +39,14 @@ for name in names:
     tabs = [KM.pose_tables(sc.rig, KM.PoseSpec.make(sc.poses[f])) for f in range(frames)]
     cams = [[fp.camera(c) for c in sc.cameras[f]] for f in range(frames)]
 
+    sep = os.environ.get("ARTEMIS_VIEWS_SEPARATE") == "1"  # one render launch per view
+
     def step(f):
         pose = KM.PoseSpec.make(sc.poses[f])
+        if len(cams[f]) > 1 and not sep:  # all views of the pose in one render launch
+            fp.run_views(pose, cams[f], lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep,
+                         tables=tabs[f])
+            return
         for v, cam in enumerate(cams[f]):
             fp.run(pose, cam, lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep, tables=tabs[f],
                    reuse_tree=v > 0)

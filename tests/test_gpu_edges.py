@@ -145,3 +145,27 @@ def test_tile_order_does_not_change_the_maps(mini):
             fp.set_tile_order(61, 45, np.zeros(n, np.int32))  # not a permutation
     finally:
         fp.close()
+
+
+@pytest.mark.parametrize("maps64", [False, True])
+def test_views_in_one_launch_equal_separate_renders(maps64):
+    """run_views (one render launch, the views' tiles interleaved) gives
+    each view exactly what its own render gives."""
+    from paper_2202_05628_b200.frame import FramePipeline
+
+    sc = S.make_scene("c1", resolution=64, image=(53, 37))
+    fp = FramePipeline.from_scene(sc)
+    try:
+        pose = KM.PoseSpec.make(sc.poses[0])
+        cams = sc.cameras[0][:5]
+        sep = []
+        for i, cam in enumerate(cams):
+            sep.append([x.clone() for x in fp.run(pose, cam, graph=False, maps64=maps64,
+                                                   reuse_tree=i > 0)])
+        for graph in (False, True, True):
+            got = fp.run_views(pose, cams, graph=graph, maps64=maps64)
+            fp.stream.synchronize()
+            for a, b in zip(sep, got):
+                assert all(torch.equal(x, y) for x, y in zip(a, b))
+    finally:
+        fp.close()
