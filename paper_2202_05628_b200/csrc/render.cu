@@ -205,15 +205,17 @@ __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t 
 // the reference's `lt0 <= rt0` comparison yields (_core.pyx:345). Internal
 // tests use the fp32 filter; emitted leaves get exact fp64 intervals.
 // kRays: 0 = explicit ray arrays (fp64 maps), 1 = in-kernel camera rays with
-// fp32 alpha/depth maps (frame pipeline), 2 = camera rays with fp64 maps
+// fp32 alpha/depth maps (frame pipeline), 2 = camera rays with fp64 maps,
+// 3 / 4 = as 1 / 2 over several views in one launch (run_views)
 template <int kDeg, int kMode, int kRays, bool kVec, bool kDDA>
 __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_kernel(RenderArgs p) {
     constexpr bool kCamera = kRays != 0;
+    constexpr bool kMulti = kRays >= 3;  // several views per launch (run_views)
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
-    using T0 = typename std::conditional<kRays == 1, float, double>::type;
-    constexpr int kQueueBytes = queue_bytes(kRays == 1);
+    using T0 = typename std::conditional<kRays == 1 || kRays == 3, float, double>::type;
+    constexpr int kQueueBytes = queue_bytes(kRays == 1 || kRays == 3);
     constexpr int kStackB = stack_bytes(kDDA);
     unsigned char *qbase = s_raw + kStackB;
     uint32_t *q_id = reinterpret_cast<uint32_t *>(qbase);                            // leaf, then row
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // camera mode: the tiles of all views interleave in the ray queue (tile t
     // of view 0, of view 1, ..., then tile t + 1), so the views' rays over
     // the same leaves are in flight together and share their FLUT rows in L2
-    const int nv = kCamera && p.n_views > 1 ? p.n_views : 1;
+    const int nv = kMulti ? p.n_views : 1;
     const int64_t n_ids = kCamera ? (tstart < n_tiles ? (n_tiles - tstart + tstride - 1) / tstride : 0) * 32 * nv
                                   : p.n_rays;
     const unsigned lt = lanemask_lt();
@@ -477,9 +479,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         double dw[3];
         if (kCamera) {
             const int64_t gi = id >> 5;
-            rv = nv > 1 ? (int)(gi % nv) : 0;
+            if (kMulti) rv = (int)(gi % nv);
             const artemis_camera &cam = p.cam[rv];
-            const int64_t t = tstart + (nv > 1 ? gi / nv : gi) * tstride;
+            const int64_t t = tstart + (kMulti ? gi / nv : gi) * tstride;
             const int64_t tile = order ? (int64_t)__ldg(order + t) : t;
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             if (kMode == kCount) {
                 p.counts[ray] = hits;
             } else {
-                if (nv > 1) {  // per-view maps
+                if (kMulti) {  // per-view maps
                     if (p.A64) {
                         static_cast<double *>(p.Av[rv])[ray] = acc;
                         static_cast<double *>(p.Dv[rv])[ray] = depth;
@@ -877,7 +879,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 fm &= fm - 1;
                 const int64_t r = __shfl_sync(0xffffffffu, ray, s);
                 float *Fo = p.F;
-                if (kCamera && nv > 1) Fo = p.Fv[__shfl_sync(0xffffffffu, rv, s)];
+                if (kMulti) Fo = p.Fv[__shfl_sync(0xffffffffu, rv, s)];
                 for (int c = lane; c < C; c += 32) {
                     Fo[r * C + c] = feat[s * cp + c];
                     feat[s * cp + c] = FeatT(0);
@@ -899,7 +901,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
     const size_t feat_bytes = 4;
-    const size_t smem = stack_bytes(kDDA) + queue_bytes(kRays == 1) +
+    const size_t smem = stack_bytes(kDDA) + queue_bytes(kRays == 1 || kRays == 3) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * feat_bytes) +
                         (size_t)kRenderWarps * 32 * kQCap * (2 + 4) + (size_t)kRenderThreads * 6 * 8;
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
@@ -1049,6 +1051,11 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         a.D32 = static_cast<float *>(D);
     }
     const int64_t warps = (int64_t)a.tiles_x * ((height + 3) / 4) * (n_views > 1 ? n_views : 1);
+    // kRays: 1 / 2 camera rays with float / double maps, 3 / 4 the same over
+    // several views
+    if (n_views > 1)
+        return maps64 ? launch_render_deg<kRender, 4>(shade->degree, a, warps, st)
+                      : launch_render_deg<kRender, 3>(shade->degree, a, warps, st);
     return maps64 ? launch_render_deg<kRender, 2>(shade->degree, a, warps, st)
                   : launch_render_deg<kRender, 1>(shade->degree, a, warps, st);
 }
