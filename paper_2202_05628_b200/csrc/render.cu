@@ -41,7 +41,7 @@ namespace artemis {
 #define ARTEMIS_QCAP 6
 #endif
 #ifndef ARTEMIS_QTHRESH
-#define ARTEMIS_QTHRESH 64
+#define ARTEMIS_QTHRESH 48
 #endif
 #ifndef ARTEMIS_MIN_BLOCKS
 #define ARTEMIS_MIN_BLOCKS 4
