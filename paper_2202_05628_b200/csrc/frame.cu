@@ -38,7 +38,8 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
-                  float *const *Fv, void *const *Av, void *const *Dv, cudaStream_t st);
+                  float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
+                  cudaStream_t st);
 
 // per-view outputs of a multi-view frame (artemis_frame_run_views)
 struct ViewOut {
@@ -161,7 +162,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, st);
+                           vo.D, f->n, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -236,7 +237,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                sigma_dep, flags & 1, (flags & 8) ? 1 : 0, vo.F[v], vo.A[v],
                                vo.D[v], reinterpret_cast<unsigned long long *>(f->counters + 2),
                                order, &f->params->order_on, nullptr, 1, nullptr, nullptr, nullptr,
-                               st);
+                               f->n, st);
         }
         launches += vo.n - 1;
     } else {
@@ -244,7 +245,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, st);
+                           vo.D, f->n, st);
     }
     mark(5);
     launches += 1;

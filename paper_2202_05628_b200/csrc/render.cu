@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const uint4 L2 = __ldg(p.leaves + 2 * (size_t)q_id[qi] + 1);
                 const uint32_t fidx = L.w;
 #if ARTEMIS_ROW_PREFETCH
-                {   // the row's 9 x 128 B lines are read in phase C
+                if (!p.no_row_prefetch) {  // the row's 9 x 128 B lines are read in phase C
                     const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
                     for (int off = 0; off < (ARTEMIS_ROW_PREFETCH == 2 ? 1 : p.coef_stride * 4); off += 128)
                         prefetch_l2(row + off);
@@ -992,8 +992,21 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
-                  float *const *Fv, void *const *Av, void *const *Dv, cudaStream_t st) {
+                  float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
+                  cudaStream_t st) {
     RenderArgs a{};
+    {   // a FLUT that fits in half the L2 stays resident: prefetching its rows only costs
+        static int l2 = 0;
+        if (!l2) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+            if (l2 <= 0) l2 = 126 << 20;
+        }
+        const int stride = shade->coef_stride > 0 ? shade->coef_stride
+                                                  : (shade->degree + 1) * (shade->degree + 1) * shade->channels;
+        a.no_row_prefetch = flut_rows > 0 && (double)flut_rows * stride * 4.0 <= 0.5 * l2;
+    }
     if (n_views > 1) {  // several views of one tree in one launch (unsharded, own outputs)
         if (n_views > kMaxViews || sharded || (peer_out && peer_out[0])) return ARTEMIS_ERR_ARG;
         const int64_t n = (int64_t)width * height;

@@ -49,6 +49,7 @@ struct RenderArgs {
     float coord_max;  // upper bound of every box coordinate (grid resolution)
     double sigma_dep;
     int early_stop;
+    int no_row_prefetch;  // skip the L2 prefetch of queued rows (FLUT already L2-resident)
     // outputs
     float *F;
     double *A64, *D64;
