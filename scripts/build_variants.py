@@ -25,6 +25,7 @@ VARIANTS = {
     "b6": ("ARTEMIS_MIN_BLOCKS=6",),
     "t96": ("ARTEMIS_QTHRESH=96",),
     "t32": ("ARTEMIS_QTHRESH=32",),
+    "t64": ("ARTEMIS_QTHRESH=64",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
