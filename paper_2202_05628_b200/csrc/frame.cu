@@ -39,7 +39,9 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
                   float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
-                  cudaStream_t st);
+                  int outputs_ready, cudaStream_t st);
+int render_clear_outputs(float *F, void *A, void *D, int64_t n, int channels, int sharded,
+                         int maps64, cudaStream_t st);
 
 // per-view outputs of a multi-view frame (artemis_frame_run_views)
 struct ViewOut {
@@ -122,6 +124,10 @@ struct artemis_frame_s {
     // per render launch (order_slot, enqueue_frame); row-major and one launch
     // per view beyond
     int small_flut = 1;
+    // second stream of the frame (output clearing, brick map) and its
+    // fork / mid / join events
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr;
     // tile-sharded frames written straight into another rank's full-frame
     // F / alpha / depth (peer memory over NVLink): artemis_frame_set_output_peer
     void *peer_out[3] = {nullptr, nullptr, nullptr};
@@ -137,6 +143,23 @@ int dev_alloc(T **p, size_t bytes) {
         set_cuda_error(e);
         return ARTEMIS_ERR_OOM;
     }
+    return ARTEMIS_OK;
+}
+
+// The occupancy brick map, on the side stream once the live codes exist.
+int bricks_on_side(artemis_frame f, cudaStream_t st) {
+    ARTEMIS_TRY(cudaEventRecord(f->ev_mid, st));
+    ARTEMIS_TRY(cudaStreamWaitEvent(f->side, f->ev_mid, 0));
+    const int org[3] = {0, 0, 0};
+    int rc = f->key_bytes == 4
+                 ? build_bricks<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
+                                          f->n, org, f->bdims, f->btable, f->brecs, f->bmeta,
+                                          f->bmeta + 1, f->side)
+                 : build_bricks<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n, org,
+                                     f->bdims, f->btable, f->brecs, f->bmeta, f->bmeta + 1,
+                                     f->side);
+    if (rc) return rc;
+    ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));
     return ARTEMIS_OK;
 }
 
@@ -162,13 +185,28 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, f->n, st);
+                           vo.D, f->n, 0, st);
         mark(5);
         f->launches = 1;
         return rc;
     }
     // counters: [0] in-bounds, [1] live leaves, [2..3] render ray queue (u64)
     ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 4 * sizeof(int32_t), st));
+    // side stream: the outputs are cleared while the rebuild runs, and the
+    // brick map is built beside the Karras tree (both only read the live
+    // codes); joined before the render
+    ARTEMIS_TRY(cudaEventRecord(f->ev_fork, st));
+    ARTEMIS_TRY(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    {
+        const int64_t px = (int64_t)width * height;
+        const bool peer = sharded && f->peer_out[0];
+        for (int v = 0; v < vo.n && !peer; ++v) {
+            rc = render_clear_outputs(vo.n > 1 ? vo.F[v] : F, vo.n > 1 ? vo.A[v] : A,
+                                      vo.n > 1 ? vo.D[v] : D, px, as.channels,
+                                      vo.n > 1 ? 0 : sharded, (flags & 8) ? 1 : 0, f->side);
+            if (rc) return rc;
+        }
+    }
     rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,
                        identity ? 1 : n_joints, f->lo, f->cell, as.resolution, f->key_bytes,
                        f->keys, f->vals, f->rot_joint, f->counters, f->sentinel, identity, st);
@@ -191,6 +229,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                nullptr, f->counters + 1, f->resolve_ws, f->resolve_ws_bytes, st);
         if (rc) return rc;
         mark(3);
+        rc = bricks_on_side(f, st);
+        if (rc) return rc;
         rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
                                          f->n, write_ref ? f->left : nullptr, f->right, f->bmin,
                                          f->bsize, nullptr, f->leaves, f->winners, as.sigma,
@@ -205,23 +245,16 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                           f->resolve_ws, f->resolve_ws_bytes, st);
         if (rc) return rc;
         mark(3);
+        rc = bricks_on_side(f, st);
+        if (rc) return rc;
         rc = launch_build_tree<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n,
                                     write_ref ? f->left : nullptr, f->right, f->bmin, f->bsize,
                                     nullptr, f->leaves, f->winners, as.sigma, f->rot_joint,
                                     nullptr, st);
     }
     if (rc) return rc;
-    {
-        const int org[3] = {0, 0, 0};
-        rc = f->key_bytes == 4
-                 ? build_bricks<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1, f->n,
-                                          org, f->bdims, f->btable, f->brecs, f->bmeta, f->bmeta + 1,
-                                          st)
-                 : build_bricks<u64>((const u64 *)f->live_codes, 0, f->counters + 1, f->n, org,
-                                     f->bdims, f->btable, f->brecs, f->bmeta, f->bmeta + 1, st);
-        if (rc) return rc;
-        launches += 2;
-    }
+    ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
+    launches += 2;  // the brick passes (side stream)
     mark(4);
     const int passes = f->key_bits <= 0 ? 1 : (f->key_bits + 7) / 8;
     launches += 2 + passes + 3 + 1;  // + 2 brick passes counted above
@@ -237,7 +270,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                sigma_dep, flags & 1, (flags & 8) ? 1 : 0, vo.F[v], vo.A[v],
                                vo.D[v], reinterpret_cast<unsigned long long *>(f->counters + 2),
                                order, &f->params->order_on, nullptr, 1, nullptr, nullptr, nullptr,
-                               f->n, st);
+                               f->n, 1, st);
         }
         launches += vo.n - 1;
     } else {
@@ -245,7 +278,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, f->n, st);
+                           vo.D, f->n, 1, st);
     }
     mark(5);
     launches += 1;
@@ -412,6 +445,16 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->vals_sorted, n * 4);
     rc = rc ? rc : dev_alloc(&f->winners, n * 4);
     rc = rc ? rc : dev_alloc(&f->rot_joint, n * 4);
+    if (!rc) {
+        cudaError_t e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_mid, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            set_cuda_error(e);
+            rc = ARTEMIS_ERR_CUDA;
+        }
+    }
     rc = rc ? rc : dev_alloc(&f->counters, 64);
     if (!rc && cudaMemset(f->counters, 0, 64) != cudaSuccess) rc = ARTEMIS_ERR_CUDA;
     rc = rc ? rc : dev_alloc(&f->left, n * 4);
@@ -467,6 +510,9 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     if (f->staging) cudaFreeHost(f->staging);
     for (auto &o : f->orders)
         if (o.dev) cudaFree(o.dev);
+    for (cudaEvent_t e : {f->ev_fork, f->ev_mid, f->ev_join})
+        if (e) cudaEventDestroy(e);
+    if (f->side) cudaStreamDestroy(f->side);
 
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,

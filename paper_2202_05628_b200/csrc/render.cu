@@ -985,6 +985,25 @@ __global__ void fill_alpha_depth(T *A, T *D, int64_t n) {
     }
 }
 
+// Output clearing of render_camera, for callers that run it ahead on another
+// stream (frame.cu: concurrent with the rebuild): F zero, and for sharded
+// frames alpha 0 / depth +inf (other ranks' pixels).
+int render_clear_outputs(float *F, void *A, void *D, int64_t n, int channels, int sharded,
+                         int maps64, cudaStream_t st) {
+    ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * channels * sizeof(float), st));
+    if (sharded) {
+        const int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148);
+        if (maps64)
+            fill_alpha_depth<double><<<g, 256, 0, st>>>(static_cast<double *>(A),
+                                                        static_cast<double *>(D), n);
+        else
+            fill_alpha_depth<float><<<g, 256, 0, st>>>(static_cast<float *>(A),
+                                                       static_cast<float *>(D), n);
+        return ARTEMIS_LAUNCHED();
+    }
+    return ARTEMIS_OK;
+}
+
 // Device-pipeline render with in-kernel camera rays (frame.cu). maps64:
 // alpha/depth are double (exact fp64 maps, as the API path) instead of float.
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
@@ -993,7 +1012,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
                   float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
-                  cudaStream_t st) {
+                  int outputs_ready, cudaStream_t st) {
     RenderArgs a{};
     {   // a FLUT that fits in half the L2 stays resident: prefetching its rows only costs
         static int l2 = 0;
@@ -1011,7 +1030,8 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         if (n_views > kMaxViews || sharded || (peer_out && peer_out[0])) return ARTEMIS_ERR_ARG;
         const int64_t n = (int64_t)width * height;
         for (int v = 0; v < n_views; ++v) {
-            ARTEMIS_TRY(cudaMemsetAsync(Fv[v], 0, (size_t)n * shade->channels * sizeof(float), st));
+            if (!outputs_ready)
+                ARTEMIS_TRY(cudaMemsetAsync(Fv[v], 0, (size_t)n * shade->channels * sizeof(float), st));
             a.Fv[v] = Fv[v];
             a.Av[v] = Av[v];
             a.Dv[v] = Dv[v];
@@ -1036,9 +1056,9 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         A = peer_out[1];
         D = peer_out[2];
     }
-    if (!peer && n_views <= 1)
+    if (!peer && n_views <= 1 && !outputs_ready)
         ARTEMIS_TRY(cudaMemsetAsync(F, 0, (size_t)n * shade->channels * sizeof(float), st));
-    if (sharded && !peer) {  // pixels of other ranks' tiles: alpha 0, depth +inf
+    if (sharded && !peer && !outputs_ready) {  // pixels of other ranks' tiles: alpha 0, depth +inf
         const int g = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * 148);
         if (maps64)
             fill_alpha_depth<double><<<g, 256, 0, st>>>(static_cast<double *>(A),
