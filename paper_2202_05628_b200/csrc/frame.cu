@@ -9,16 +9,19 @@
 //   render_view          render.py:322-363     -> render_kernel, camera rays in-kernel
 // The in-bounds and live counts never leave the device: every kernel after
 // the warp sizes its grid for the worst case and reads the count.
-// Per-frame inputs (joint deltas, inverse rotations, camera) are copied into
-// a device parameter block before the graph launch, so the graph itself is
-// pose- and camera-independent.
+// Per-frame inputs (joint deltas, inverse rotations, cameras, tile-order
+// flag) are copied into a device parameter block before the graph launch,
+// so the graph itself is pose- and camera-independent. A side stream clears
+// the outputs and builds the occupancy brick map while the main stream runs
+// the rebuild; several views of one pose render in one launch
+// (artemis_frame_run_views).
+#include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
-#include <math.h>
-
 #include <algorithm>
-#include <string>
 #include <numeric>
+#include <string>
 #include <vector>
 
 #include "bricks.cuh"
