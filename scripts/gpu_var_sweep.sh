@@ -1,3 +1,5 @@
+# Library-variant sweep: bench.py (configs[2]) plus configs[4] and configs[1] per variant:
+#   VARIANTS="base x y" bash scripts/gpu_var_sweep.sh
 cd "$GRAFT_REPO_ROOT"
 for v in ${VARIANTS:-base}; do
   if [ $v = base ]; then LP=$PWD/paper_2202_05628_b200/libartemis.so; else LP=$PWD/variants/libartemis_$v.so; fi
