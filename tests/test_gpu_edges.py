@@ -169,3 +169,23 @@ def test_views_in_one_launch_equal_separate_renders(maps64):
                 assert all(torch.equal(x, y) for x, y in zip(a, b))
     finally:
         fp.close()
+
+
+def test_configs1_views_one_launch_full_size():
+    """configs[1] at full size: the 8 views rendered in one launch equal
+    their separate renders bit for bit."""
+    from paper_2202_05628_b200.frame import FramePipeline
+
+    sc = S.make_scene("c1")
+    fp = FramePipeline.from_scene(sc)
+    try:
+        pose = KM.PoseSpec.make(sc.poses[0])
+        sep = [[x.clone() for x in fp.run(pose, cam, graph=False, reuse_tree=i > 0)]
+               for i, cam in enumerate(sc.cameras[0])]
+        got = fp.run_views(pose, sc.cameras[0], graph=True)
+        fp.stream.synchronize()
+        assert len(got) == 8
+        for a, b in zip(sep, got):
+            assert all(torch.equal(x, y) for x, y in zip(a, b))
+    finally:
+        fp.close()
