@@ -331,7 +331,8 @@ int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double
                       double sigma_dep, int flags, float *F, void *alpha, void *depth,
                       artemis_stream stream);
 
-/* Tile-sharded frames (camera tile_stride > 1) of this handle write their
+/* (no reference counterpart: multi-GPU assembly) Tile-sharded frames
+ * (camera tile_stride > 1) of this handle write their
  * pixels straight into F / alpha / depth -- the destination rank's
  * full-frame buffers mapped into this process (CUDA IPC, peer access over
  * NVLink), or this rank's own on the destination -- instead of the local
@@ -341,7 +342,8 @@ int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double
  * double with ARTEMIS_FRAME_MAPS64. F == NULL restores the local outputs. */
 int artemis_frame_set_output_peer(artemis_frame frame, float *F, void *alpha, void *depth);
 
-/* Render order of the 8x4 ray tiles for one image size: `order` (HOST,
+/* (no reference counterpart: scheduling only) Render order of the 8x4 ray
+ * tiles for one image size: `order` (HOST,
  * ceil(w/8)*ceil(h/4) int32) must be a permutation of the tile indices
  * (row-major tile numbering); ARTEMIS_ERR_ARG otherwise. Without it the
  * pipeline renders centre-out while the asset's FLUT coefficients fit in
@@ -350,8 +352,9 @@ int artemis_frame_set_output_peer(artemis_frame frame, float *F, void *alpha, vo
 int artemis_frame_set_tile_order(artemis_frame frame, int width, int height,
                                  const int32_t *order);
 
-/* One pose, several views (configs[1] views, configs[4] stereo eyes): warp
- * + rebuild once, then ONE render launch over all n_views (<= 8) cameras of
+/* replaces one animvox/render.py:154-178 posed_octree followed by one
+ * render_view (render.py:322-363) per camera. One pose, several views
+ * (configs[1] views, configs[4] stereo eyes): warp + rebuild once, then ONE render launch over all n_views (<= 8) cameras of
  * the same image size, their 8x4 tiles interleaved in the ray queue so the
  * views' rays over the same leaves are in flight together and share the
  * FLUT rows in L2. Outputs per view: F[v], alpha[v], depth[v] (as
