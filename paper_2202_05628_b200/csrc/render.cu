@@ -38,7 +38,7 @@ namespace artemis {
 #define ARTEMIS_SMEM_STACK 28
 #endif
 #ifndef ARTEMIS_QCAP
-#define ARTEMIS_QCAP 6
+#define ARTEMIS_QCAP 5
 #endif
 #ifndef ARTEMIS_QTHRESH
 #define ARTEMIS_QTHRESH 48

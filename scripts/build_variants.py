@@ -25,6 +25,8 @@ VARIANTS = {
     "b6": ("ARTEMIS_MIN_BLOCKS=6",),
     "t96": ("ARTEMIS_QTHRESH=96",),
     "t32": ("ARTEMIS_QTHRESH=32",),
+    "q5t48": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=48"),
+    "q5t40": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=40"),
     "t64": ("ARTEMIS_QTHRESH=64",),
 }
 names = sys.argv[1:] or list(VARIANTS)
