@@ -27,6 +27,8 @@ VARIANTS = {
     "t32": ("ARTEMIS_QTHRESH=32",),
     "q5t48": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=48"),
     "q5t40": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=40"),
+    "q5t44": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=44"),
+    "q5t56": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=56"),
     "t64": ("ARTEMIS_QTHRESH=64",),
 }
 names = sys.argv[1:] or list(VARIANTS)
