@@ -339,8 +339,12 @@ int artemis_frame_run(artemis_frame frame, const double *joint_aff, const double
  * outputs (left untouched). The destination initialises them (F 0, alpha 0,
  * depth +inf) before any rank renders; each rank writes exactly its own
  * tiles, so the assembled frame needs no gather. alpha/depth are float, or
- * double with ARTEMIS_FRAME_MAPS64. F == NULL restores the local outputs. */
-int artemis_frame_set_output_peer(artemis_frame frame, float *F, void *alpha, void *depth);
+ * double with ARTEMIS_FRAME_MAPS64. F == NULL restores the local outputs.
+ * n_pixels / maps64 describe the peer maps: a sharded artemis_frame_run whose
+ * image size or map type differs returns ARTEMIS_ERR_ARG (no stores past the
+ * end of another rank's buffers). */
+int artemis_frame_set_output_peer(artemis_frame frame, float *F, void *alpha, void *depth,
+                                  int64_t n_pixels, int maps64);
 
 /* (no reference counterpart: scheduling only) Render order of the 8x4 ray
  * tiles for one image size: `order` (HOST,
@@ -500,6 +504,17 @@ int artemis_tiles_pack(const float *F, const float *alpha, const float *depth, i
 int artemis_tiles_unpack(const float *packed, int width, int height, int channels,
                          int tile_start, int tile_stride, float *F, float *alpha, float *depth,
                          artemis_stream stream);
+
+/* artemis_host_checksum (host, synchronous): 128-bit content digest of a
+ * HOST buffer (every byte; 64 KB blocks over up to `threads` host threads,
+ * combined in block order so the digest is thread-count independent) into
+ * out[2]. No reference counterpart: the reference re-reads its numpy
+ * arguments on every kernels.* call (_core.pyx:473-559, 562-655); the
+ * kernel-contract shim keys its device copies of the FLUT and tree by this
+ * digest so repeated calls (render.py:209-231 integrate_ray, fit.py:474-480)
+ * skip the upload while an in-place edit still takes effect. */
+int artemis_host_checksum(const void *data /* host */, size_t bytes, int threads,
+                          uint64_t *out /* host, 2 words */);
 
 /* Synchronous device -> host copy (parity helpers). */
 int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);

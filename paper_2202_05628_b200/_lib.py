@@ -107,7 +107,7 @@ _SIGS = {
     "artemis_frame_get_tree": (INT, [P, C.POINTER(FrameTree)]),
     "artemis_frame_launches": (INT, [P]),
     "artemis_frame_set_tile_order": (INT, [P, INT, INT, P]),
-    "artemis_frame_set_output_peer": (INT, [P, P, P, P]),
+    "artemis_frame_set_output_peer": (INT, [P, P, P, P, I64, INT]),
     "artemis_frame_run_views": (INT, [P, P, P, INT, P, INT, DBL, DBL, INT, P, P, P, P]),
     "artemis_copy_to_host": (INT, [P, P, SZ, P]),
     "artemis_frame_profile": (INT, [P, INT]),
@@ -138,6 +138,7 @@ _SIGS = {
     "artemis_tiles_shard_floats": (I64, [INT, INT, INT, INT, INT]),
     "artemis_tiles_pack": (INT, [P, P, P, INT, INT, INT, INT, INT, P, P]),
     "artemis_tiles_unpack": (INT, [P, INT, INT, INT, INT, INT, P, P, P, P]),
+    "artemis_host_checksum": (INT, [P, SZ, INT, P]),
 }
 
 EXPORTS = tuple(_SIGS)

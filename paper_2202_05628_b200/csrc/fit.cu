@@ -132,7 +132,7 @@ __global__ void vrt_apply_kernel(const double *__restrict__ data, int width,
     }
 }
 
-// SparseAdam on touched rows, then the density clamp of those rows
+// SparseAdam on touched rows, then the density clamp of every row
 __global__ void adam_kernel(double *__restrict__ params, double *__restrict__ m,
                             double *__restrict__ v, const double *__restrict__ grad,
                             const uint8_t *__restrict__ touched, int64_t n_rows, int width,
@@ -143,7 +143,12 @@ __global__ void adam_kernel(double *__restrict__ params, double *__restrict__ m,
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = i / width;
-        if (!touched[row]) continue;
+        if (!touched[row]) {
+            // FLUT.clamp_densities clamps the whole density column every
+            // iteration (volume.py:166-167), touched or not; np.maximum keeps NaN
+            if ((int)(i - row * width) == width - 1 && params[i] < 0.0) params[i] = 0.0;
+            continue;
+        }
         const double g = grad[i];
         const double mi = DA(DM(b1, m[i]), DM(ob1, g));
         const double vi = DA(DM(b2, v[i]), DM(DM(ob2, g), g));

@@ -134,6 +134,8 @@ struct artemis_frame_s {
     // tile-sharded frames written straight into another rank's full-frame
     // F / alpha / depth (peer memory over NVLink): artemis_frame_set_output_peer
     void *peer_out[3] = {nullptr, nullptr, nullptr};
+    int64_t peer_pixels = 0;  // size of the peer maps (pixels) and their alpha/depth type
+    int peer_maps64 = 0;
     int profile = 0;
 };
 
@@ -374,8 +376,9 @@ artemis_frame_s::OrderSlot *order_slot(artemis_frame f, int w, int h, int *rc) {
 // (F 0, alpha 0, depth +inf) before any rank renders; every rank writes only
 // its own tiles, so the assembled frame needs no gather. NULLs restore the
 // local outputs. Captured graphs are dropped (they bake the pointers).
-extern "C" int artemis_frame_set_output_peer(artemis_frame f, float *F, void *alpha, void *depth) {
-    if (!f || (F && (!alpha || !depth))) return ARTEMIS_ERR_ARG;
+extern "C" int artemis_frame_set_output_peer(artemis_frame f, float *F, void *alpha, void *depth,
+                                             int64_t n_pixels, int maps64) {
+    if (!f || (F && (!alpha || !depth || n_pixels < 1))) return ARTEMIS_ERR_ARG;
     for (auto &g : f->graphs)
         if (g.exec) {
             cudaGraphExecDestroy(g.exec);
@@ -384,6 +387,8 @@ extern "C" int artemis_frame_set_output_peer(artemis_frame f, float *F, void *al
     f->peer_out[0] = F;
     f->peer_out[1] = F ? alpha : nullptr;
     f->peer_out[2] = F ? depth : nullptr;
+    f->peer_pixels = F ? n_pixels : 0;
+    f->peer_maps64 = F ? (maps64 ? 1 : 0) : 0;
     return ARTEMIS_OK;
 }
 
@@ -573,6 +578,10 @@ static int frame_run_impl(artemis_frame f, const double *joint_aff, const double
                                     sizeof(double) * 9 * n_joints, cudaMemcpyHostToDevice, st));
     }
     const int sharded = cam->tile_stride > 1;
+    if (sharded && f->peer_out[0] &&
+        ((int64_t)cam->width * cam->height != f->peer_pixels ||
+         ((flags & 8) ? 1 : 0) != f->peer_maps64))
+        return ARTEMIS_ERR_ARG;  // the peer maps are another image size / map type
     const int32_t *order = nullptr;
     hp->order_on = 0;
     if (!sharded) {

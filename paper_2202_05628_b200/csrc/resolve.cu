@@ -66,6 +66,18 @@ __global__ void __launch_bounds__(1024) block_scan_kernel(uint32_t *counts, int6
     if (threadIdx.x == 0) *n_live = (int32_t)carry;
 }
 
+// Order of a collision group in the reference's np.lexsort((idx, -sigma,
+// code)) (rigging.py:435): larger density first, ties by lower canonical
+// index; NaN densities sort last (numpy puts NaN after every number), among
+// themselves by index. A strict total order, so exactly one entry has rank 0
+// even when densities are NaN.
+__device__ __forceinline__ bool precedes(double sa, uint32_t a, double sb, uint32_t b) {
+    const bool na = isnan(sa), nb = isnan(sb);
+    if (na != nb) return nb;  // the number precedes the NaN
+    if (na) return a < b;
+    return sa > sb || (sa == sb && a < b);
+}
+
 template <typename K, bool kPairs>
 __global__ void __launch_bounds__(kBlock) resolve_kernel(
     const K *__restrict__ codes, const uint32_t *__restrict__ idx, int64_t n_host,
@@ -101,8 +113,8 @@ __global__ void __launch_bounds__(kBlock) resolve_kernel(
     for (int64_t m = s; m < e; ++m) {
         uint32_t o = idx[m];
         double so = sigma[o];
-        if (so > sm || (so == sm && o < me)) ++rank;
-        if (so > best_s || (so == best_s && o < best)) {
+        if (precedes(so, o, sm, me)) ++rank;
+        if (precedes(so, o, best_s, best)) {
             best = o;
             best_s = so;
         }

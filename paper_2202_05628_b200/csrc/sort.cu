@@ -255,12 +255,12 @@ int sort_pairs(const K *keys_in, const uint32_t *vals_in, K *keys_out, uint32_t 
     radix_hist_kernel<K><<<hist_blocks, kThreads, 0, st>>>(keys_in, n, L.passes, hist);
     radix_scan_kernel<<<L.passes, kRadix, 0, st>>>(hist);
     const size_t stage = (size_t)kTile * (sizeof(K) + 4);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(onesweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
-        cudaFuncSetAttribute(onesweep_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
-        attr_set = true;
-    }
+    // the opt-in is per device (and context): set it on every call, as the
+    // render launches do -- it costs ~1 us and is legal during graph capture
+    ARTEMIS_TRY(cudaFuncSetAttribute(onesweep_kernel<K, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage));
+    ARTEMIS_TRY(cudaFuncSetAttribute(onesweep_kernel<K, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage));
     const K *src_k = keys_in;
     const uint32_t *src_v = vals_in;
     for (int p = 0; p < L.passes; ++p) {

@@ -501,10 +501,18 @@ class FramePipeline:
     def set_output_peer(self, F=None, alpha=None, depth=None) -> None:
         """Tile-sharded frames write their pixels into these full-frame device
         tensors (the destination rank's, mapped over CUDA IPC / NVLink)
-        instead of this pipeline's outputs; None restores the local ones."""
+        instead of this pipeline's outputs; None restores the local ones.
+        A sharded frame of another image size or map type is refused."""
+        if F is None:
+            check(_lib.lib().artemis_frame_set_output_peer(self._h, None, None, None, 0, 0),
+                  "frame_set_output_peer")
+            return
+        n = int(alpha.numel())
+        if F.numel() != n * self.channels or depth.numel() != n or depth.dtype != alpha.dtype:
+            raise ValueError("peer maps must be (n, C) F and (n,) alpha/depth of one dtype")
         check(_lib.lib().artemis_frame_set_output_peer(
-            self._h, ptr(F) if F is not None else None, ptr(alpha) if F is not None else None,
-            ptr(depth) if F is not None else None), "frame_set_output_peer")
+            self._h, ptr(F), ptr(alpha), ptr(depth), n, int(alpha.dtype == torch.float64)),
+            "frame_set_output_peer")
 
     def set_tile_order(self, width: int, height: int, order) -> None:
         """Render the 8x4 ray tiles of a width x height image in `order` (a

@@ -132,6 +132,10 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def _camera_size(camera) -> tuple[int, int]:
+    return int(camera.width), int(camera.height)
+
+
 class PeerAssembly:
     """Tile-sharded frames assembled by the render kernels themselves.
 
@@ -168,7 +172,16 @@ class PeerAssembly:
 
     def frame(self, pose, camera, **kw):
         """Render one tile-sharded frame into the root's maps; returns the
-        root's (F, alpha, depth) on the root, None elsewhere."""
+        root's (F, alpha, depth) on the root, None elsewhere. With one rank
+        the frame is rendered unsharded into the pipeline's own maps."""
+        w, h = _camera_size(camera)
+        if (w, h) != (self.width, self.height):
+            raise ValueError(f"camera is {w}x{h}; the assembly maps are "
+                             f"{self.width}x{self.height}")
+        if self.world == 1:
+            F, A, D = self.fp.run(pose, camera, maps64=self.maps64, **kw)
+            self.fp.stream.synchronize()
+            return F, A, D
         if self.rank == self.dst:
             with torch.cuda.stream(self.fp.stream):
                 self.F.zero_()

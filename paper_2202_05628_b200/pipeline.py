@@ -32,7 +32,6 @@ pointer, shape or a strided content sample).
 from __future__ import annotations
 
 import collections
-import hashlib
 import time
 import weakref
 
@@ -285,9 +284,9 @@ def render_view(octree, flut, warp, camera, options=None):
     og, dg, dw = K.camera_rays_device(R, origin, cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
                                       cam.height, lo, cell)
     rot_index, rot_inv = _rotation_tables(warp, len(flut))
-    shade = K.DeviceShading(flut.data, rot_index, rot_inv, flut.degree, flut.channels)
-    tree = K.DeviceTree(octree.codes, octree.flut_idx, octree.root, octree.left, octree.right,
-                        octree.box_min, octree.box_size, shade)
+    shade = K.shading_for(flut.data, rot_index, rot_inv, flut.degree, flut.channels)
+    tree = K.tree_for(octree.codes, octree.flut_idx, octree.root, octree.left, octree.right,
+                      octree.box_min, octree.box_size, shade)
     rays = K.DeviceRays.from_tensors(og, dg, dw, 0.0, np.inf)
     F, A, D = K.render_device(tree, shade, rays, opts.lambda_th, opts.sigma_dep, True)
     h, w = cam.height, cam.width
@@ -323,13 +322,14 @@ def _is_canonical(pose) -> bool:
 
 
 def _array_sig(a) -> tuple:
+    """Content key of one asset array: a digest of every byte under the
+    default "content" cache policy (an in-place edit, e.g. the reference's
+    FLUT.clamp_densities, is a new key), identity only under "identity"
+    (kernels.set_cache_policy; the caller then calls DEVICE_ASSETS.clear()
+    after editing)."""
     if a is None:
         return (None,)
-    a = np.asarray(a)
-    flat = a.reshape(-1)
-    step = max(1, flat.size // 4096)
-    h = hashlib.blake2b(np.ascontiguousarray(flat[::step]).tobytes(), digest_size=16)
-    return (a.__array_interface__["data"][0], a.shape, str(a.dtype), h.hexdigest())
+    return K.content_key(a)
 
 
 def _asset_sig(asset) -> tuple:

@@ -169,6 +169,29 @@ class TestDropIns:
         assert np.array_equal(res.flut_indices, win)
         assert np.array_equal(res.pairs, pairs)
 
+    def test_collision_policy_nan_densities(self, P):
+        """NaN densities sort last (np.lexsort's order): still exactly one
+        winner per live cell and every pair row written."""
+        from paper_2202_05628_b200 import types as T
+
+        rng = np.random.default_rng(22)
+        n = 3000
+        cells = (1 + rng.integers(0, 6, size=(n, 3))).astype(np.int32)
+        sigma = np.round(rng.uniform(0.0, 4.0, n), 1)
+        sigma[rng.random(n) < 0.2] = np.nan
+        warp = T.WarpResult(16, np.zeros(3), np.full(3, 1 / 16), np.zeros((n, 3)), cells,
+                            np.zeros((n, 4)), np.zeros(n, np.int32), np.eye(3)[None],
+                            np.ones(n, bool), ())
+
+        class F:
+            densities = sigma
+
+        res = P.resolve_collisions(warp, F)
+        live, win, pairs = oracle.resolve(cells, np.ones(n, bool), sigma)
+        assert np.array_equal(res.cells, live)
+        assert np.array_equal(res.flut_indices, win)
+        assert np.array_equal(res.pairs, pairs)
+
     def test_all_out_of_bounds(self, P):
         from paper_2202_05628_b200 import types as T
 

@@ -43,6 +43,30 @@ def test_sparse_adam_matches_reference(golden_fit):
     assert np.array_equal(m.cpu().numpy(), g["m3"]) and np.array_equal(v.cpu().numpy(), g["v3"])
 
 
+def test_density_clamp_covers_untouched_rows():
+    """FLUT.clamp_densities (volume.py:166-167) clamps the whole density
+    column every iteration: a user-supplied init with negative densities in
+    rows no ray touches is clamped too (np.maximum: NaN stays NaN)."""
+    L = _lib.lib()
+    rng = np.random.default_rng(4)
+    n, w = 500, 10
+    p0 = rng.normal(size=(n, w))
+    p0[7, -1] = np.nan
+    touched = (rng.random(n) < 0.3).astype(np.uint8)
+    grad = rng.normal(size=(n, w)) * touched[:, None]
+    p = dev(p0, np.float64)
+    m, v = torch.zeros_like(p), torch.zeros_like(p)
+    assert L.artemis_sparse_adam(ptr(p), ptr(m), ptr(v), ptr(dev(grad, np.float64)),
+                                 ptr(dev(touched, np.uint8)), n, w, 0.05, 0.9, 0.999, 1e-8,
+                                 0.1, 0.001, None) == 0
+    got = p.cpu().numpy()
+    untouched = touched == 0
+    assert np.array_equal(got[untouched, :-1], p0[untouched, :-1])
+    want = np.maximum(p0[untouched, -1], 0.0)
+    assert np.array_equal(got[untouched, -1], want, equal_nan=True)
+    assert np.isnan(got[7, -1]) and (got[:, -1][~np.isnan(got[:, -1])] >= 0).all()
+
+
 def test_pair_term_matches_np_add_at(golden_fit):
     g = golden_fit
     L = _lib.lib()
