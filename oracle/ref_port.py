@@ -137,9 +137,13 @@ class RefFrame:
         return (np.ascontiguousarray((o - self.sc.lo) / cell), np.ascontiguousarray(d / cell),
                 np.ascontiguousarray(d))
 
-    def frame(self, tables, cam, row_stride: int = 1):
-        """Stage seconds for one frame; render runs on every row_stride-th
-        image row and is scaled to the full image."""
+    def frame(self, tables, cams, row_stride: int = 1):
+        """Stage seconds for one posed frame: warp + rebuild once, then every
+        camera in `cams` (one camera, or a frame's views / stereo eyes)
+        rendered in full (row_stride > 1 renders every row_stride-th row
+        and scales the render time; the bench does not use it)."""
+        if not isinstance(cams, (list, tuple)):
+            cams = [cams]
         t = {}
         t0 = time.perf_counter()
         pos, cells, inside, rj, groups = self.warp(tables.delta_mats)
@@ -147,14 +151,19 @@ class RefFrame:
         live, win, pairs = self.resolve(cells, inside)
         tree = self.build(live, win)
         t2 = time.perf_counter()
-        rows = np.arange(0, cam.height, row_stride)
-        og, dg, dw = self.rays(cam, rows)
-        F, A, D = self.core.render_rays(*tree, og, dg, dw, 0.0, np.inf, self.flut, rj,
-                                        tables.rot_inv, self.sc.degree, self.sc.channels,
-                                        self.sc.lambda_th, self.sc.sigma_dep, True, self.nthreads)
-        t3 = time.perf_counter()
+        render = 0.0
+        rays = 0
+        for cam in cams:
+            t3 = time.perf_counter()
+            rows = np.arange(0, cam.height, row_stride)
+            og, dg, dw = self.rays(cam, rows)
+            self.core.render_rays(*tree, og, dg, dw, 0.0, np.inf, self.flut, rj,
+                                  tables.rot_inv, self.sc.degree, self.sc.channels,
+                                  self.sc.lambda_th, self.sc.sigma_dep, True, self.nthreads)
+            render += (time.perf_counter() - t3) * cam.height / rows.size
+            rays += int(og.shape[0])
         t["warp"] = t1 - t0
         t["build-octree"] = t2 - t1
-        t["volume-render"] = (t3 - t2) * cam.height / rows.size
-        t["rays_sampled"] = int(og.shape[0])
+        t["volume-render"] = render
+        t["rays_sampled"] = rays
         return t

@@ -318,7 +318,7 @@ def content_key(a, dtype=None) -> tuple:
     return (arr.shape, str(arr.dtype), int(out[0]), int(out[1]))
 
 
-def _lru_get(cache, key, capacity, make):
+def _lru_get(cache, key, capacity, make, on_evict=None):
     ent = cache.get(key)
     if ent is not None:
         cache.move_to_end(key)
@@ -326,7 +326,9 @@ def _lru_get(cache, key, capacity, make):
         return ent
     _STATS["misses"] += 1
     while len(cache) >= capacity:
-        cache.popitem(last=False)
+        old, _ = cache.popitem(last=False)
+        if on_evict is not None:
+            on_evict(old)
     ent = make()
     _STATS["h2d_bytes"] += getattr(ent, "h2d_bytes", 0)
     cache[key] = ent
@@ -341,21 +343,41 @@ def shading_for(flut, rot_index, rot_inv, degree, channels):
     key = (content_key(fl), content_key(rot_index, np.int32), content_key(rot_inv, np.float64),
            int(degree), int(channels))
     sh = _lru_get(_SHADE_CACHE, key, SHADE_CAPACITY,
-                  lambda: DeviceShading(fl, rot_index, rot_inv, degree, channels))
+                  lambda: DeviceShading(fl, rot_index, rot_inv, degree, channels),
+                  on_evict=_drop_trees_of)
     sh.key = key
     return sh
 
 
-def tree_for(codes, flut_idx, root, left, right, box_min, box_size, shade):
+def _drop_trees_of(shade_key) -> None:
+    """Trees embed their shading's density/rotation (and keep it alive):
+    they leave the cache with it."""
+    for k in [k for k in _TREE_CACHE if k[1] == shade_key]:
+        del _TREE_CACHE[k]
+
+
+def tree_for(codes, flut_idx, root, left, right, box_min, box_size, shade, any_shade=False):
     """Cached DeviceTree (packed nodes, leaf records, brick map) of a
-    reference-layout tree; leaf records embed `shade`'s density/rotation."""
-    key = (content_key(codes, np.uint64), content_key(flut_idx, np.uint32), int(root),
-           content_key(left, np.int32), content_key(right, np.int32),
-           content_key(box_min, np.int32), content_key(box_size, np.int32), shade.key,
-           DeviceTree.MAX_BRICK_TABLE)
-    return _lru_get(_TREE_CACHE, key, TREE_CAPACITY,
+    reference-layout tree; leaf records embed `shade`'s density/rotation.
+    any_shade: a traversal-only caller takes a cached tree of the same
+    arrays built for any shading (the walk never reads those fields)."""
+    tkey = (content_key(codes, np.uint64), content_key(flut_idx, np.uint32), int(root),
+            content_key(left, np.int32), content_key(right, np.int32),
+            content_key(box_min, np.int32), content_key(box_size, np.int32),
+            DeviceTree.MAX_BRICK_TABLE)
+    if any_shade:
+        for key in reversed(_TREE_CACHE):
+            if key[0] == tkey:
+                _TREE_CACHE.move_to_end(key)
+                _STATS["hits"] += 1
+                return _TREE_CACHE[key]
+        if shade is None:
+            return None
+    tree = _lru_get(_TREE_CACHE, (tkey, shade.key), TREE_CAPACITY,
                     lambda: DeviceTree(codes, flut_idx, root, left, right, box_min, box_size,
                                        shade))
+    tree.shade = shade
+    return tree
 
 
 def _trace_shading(rows: int):
@@ -451,8 +473,12 @@ def traverse_ray(codes, flut_idx, root, left, right, box_min, box_size, origin_g
     fi = np.asarray(flut_idx)
     rows = int(fi.max()) + 1 if fi.size else 1
     # trace-only: zero density and a 1-channel degree-0 table (no shading work)
-    shade = _trace_shading(rows)
-    tree = tree_for(codes, flut_idx, root, left, right, box_min, box_size, shade)
+    tree = tree_for(codes, flut_idx, root, left, right, box_min, box_size, None, any_shade=True)
+    if tree is not None:  # a cached tree of these arrays: its shading serves the trace
+        shade = tree.shade
+    else:
+        shade = _trace_shading(rows)
+        tree = tree_for(codes, flut_idx, root, left, right, box_min, box_size, shade)
     rays = DeviceRays(np.asarray(origin_g).reshape(1, 3), np.asarray(dir_g).reshape(1, 3), None,
                       t_min, t_max)
     _, _, _, hi, h0, h1 = forward_fit_device(tree, shade, rays)
