@@ -11,6 +11,7 @@ to the GPU box (git-ignored, not gpurun-ignored).
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -39,12 +40,35 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+HASH_FILE = LIB + ".srchash"
+
+
+def source_hash(defines: tuple = ()) -> str:
+    """SHA-256 over every source the library is built from (csrc/*.cu, *.cuh,
+    include/artemis.h), the compile flags and the nvcc version."""
+    h = hashlib.sha256()
+    deps = sorted(sources() + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  [os.path.join(INCLUDE, "artemis.h")])
+    for p in deps:
+        h.update(os.path.relpath(p, REPO).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(ARCH + FLAGS + [f"-D{d}" for d in defines]).encode())
+    try:
+        h.update(subprocess.run([nvcc(), "--version"], capture_output=True, text=True).stdout
+                 .encode())
+    except (OSError, RuntimeError):
+        pass
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    """The in-tree library is rebuilt unless it was built from exactly the
+    current sources (a content hash, not file times)."""
+    if not os.path.exists(LIB) or not os.path.exists(HASH_FILE):
         return True
-    t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "artemis.h")]
-    return any(os.path.getmtime(p) > t for p in deps)
+    with open(HASH_FILE) as fh:
+        return fh.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
@@ -80,6 +104,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         if out is None:
             with open(os.path.join(HERE, "ptxas.log"), "w") as fh:
                 fh.write("\n".join(logs))
+            with open(HASH_FILE, "w") as fh:
+                fh.write(source_hash() + "\n")
     return target
 
 

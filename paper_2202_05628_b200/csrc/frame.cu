@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "bricks.cuh"
 #include "common.cuh"
 #include "render_common.cuh"
@@ -168,6 +170,28 @@ int bricks_on_side(artemis_frame f, cudaStream_t st) {
     return ARTEMIS_OK;
 }
 
+// NVTX ranges around the stages a frame enqueues (warp, sort, resolve,
+// build, render): host-side ranges, so in eager runs they bracket each
+// stage's launches on an nsys/ncu timeline; a graph replay shows one range
+// per capture. No-ops without a tool attached.
+struct NvtxStages {
+    bool open = false;
+    void next(int k) {
+        static const char *names[5] = {"artemis warp", "artemis sort", "artemis resolve",
+                                       "artemis build", "artemis render"};
+        close();
+        if (k < 5) {
+            nvtxRangePushA(names[k]);
+            open = true;
+        }
+    }
+    void close() {
+        if (open) nvtxRangePop();
+        open = false;
+    }
+    ~NvtxStages() { close(); }
+};
+
 int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int height,
                   int sharded, double lambda_th, double sigma_dep, int flags, float *F, void *A,
                   void *D, const int32_t *order, const ViewOut &vo, cudaStream_t st) {
@@ -175,8 +199,10 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     int rc;
     int launches = 0;
     const bool prof = f->profile && !(flags & 2);
+    NvtxStages nvtx;
     auto mark = [&](int k) {
         if (prof) cudaEventRecord(f->ev[k], st);
+        nvtx.next(k);
     };
     mark(0);
     if (flags & 16) {  // ARTEMIS_FRAME_REUSE_TREE: another view of the last posed tree
