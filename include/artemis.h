@@ -516,6 +516,11 @@ int artemis_tiles_unpack(const float *packed, int width, int height, int channel
 int artemis_host_checksum(const void *data /* host */, size_t bytes, int threads,
                           uint64_t *out /* host, 2 words */);
 
+/* Test hook (no reference counterpart): cap the persistent render grid at
+ * max_blocks CTAs (0 = automatic). The maps must not depend on it -- the
+ * race/determinism tests vary it to change the ray-to-warp schedule. */
+int artemis_debug_set_render_blocks(int max_blocks);
+
 /* Synchronous device -> host copy (parity helpers). */
 int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);
 

@@ -3,12 +3,31 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "artemis.h"
 
 namespace artemis {
 
 typedef unsigned long long u64;
+
+// ---- debug checks (scripts/build_variants.py "checks": -DARTEMIS_DEBUG_CHECKS)
+// compute-sanitizer is not available on the GPU pool, so index bounds of the
+// shared-memory queues, stacks and scatter targets are asserted in a checking
+// build instead; a violation prints its site and traps.
+#ifdef ARTEMIS_DEBUG_CHECKS
+#define ARTEMIS_DCHECK(c)                                                          \
+    do {                                                                           \
+        if (!(c)) {                                                                \
+            printf("ARTEMIS_DCHECK failed: %s at %s:%d\n", #c, __FILE__, __LINE__); \
+            __trap();                                                              \
+        }                                                                          \
+    } while (0)
+#else
+#define ARTEMIS_DCHECK(c) \
+    do {                  \
+    } while (0)
+#endif
 
 // ---- status plumbing ------------------------------------------------------
 void set_cuda_error(cudaError_t e);

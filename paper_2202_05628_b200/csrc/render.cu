@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     bool queue_open = true;
 
     auto push = [&](int v) {
+        ARTEMIS_DCHECK(top < kStack);
         if (top < kSmemStack)
             s_stack[top * kRenderThreads + tid] = v;
         else
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         return top < kSmemStack ? s_stack[top * kRenderThreads + tid] : ovf[top - kSmemStack];
     };
     auto enqueue = [&](int leaf) {
+        ARTEMIS_DCHECK(nq < kQCap && leaf >= 0 && leaf < n_leaves);
         q_id[nq * kRenderThreads + tid] = (uint32_t)leaf;
         ++nq;
         prefetch_l2(p.leaves + 2 * (size_t)leaf);  // its record is read in phase B1
@@ -321,6 +323,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // the cell walk knows the exact interval already: t0, and t1 - t0 (or t1
     // for the CSR trace)
     auto enqueue_hit = [&](uint32_t leaf, double t0, double t1) {
+        ARTEMIS_DCHECK(nq < kQCap && (int64_t)leaf < n_leaves);
         const int qi = nq * kRenderThreads + tid;
         q_id[qi] = leaf;
         q_t0[qi] = (T0)t0;
@@ -487,6 +490,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
             const int py = (int)(tile / p.tiles_x) * 4 + (sl >> 3);
             if (py < cam.height && px < cam.width) {
+                ARTEMIS_DCHECK(tile >= 0 && tile < n_tiles);
                 ray = (int64_t)py * cam.width + px;
                 camera_ray(cam, px, py, og, dg, dw);
             }
@@ -623,6 +627,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         for (int k = 0; k < kQCap; ++k) {
             const unsigned m = __ballot_sync(0xffffffffu, nq > k);
             if (!m) break;
+            ARTEMIS_DCHECK(total + __popc(m) <= 32 * kQCap);
             if (nq > k) wl[total + __popc(m & lt)] = (uint16_t)(lane | (k << 5));
             total += __popc(m);
         }
@@ -643,6 +648,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const uint4 L = __ldg(p.leaves + 2 * (size_t)q_id[qi]);
                 const uint4 L2 = __ldg(p.leaves + 2 * (size_t)q_id[qi] + 1);
                 const uint32_t fidx = L.w;
+                ARTEMIS_DCHECK(p.n_rows <= 0 || (int64_t)fidx < p.n_rows);
 #if ARTEMIS_ROW_PREFETCH
                 if (!p.no_row_prefetch) {  // the row's 9 x 128 B lines are read in phase C
                     const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
@@ -896,6 +902,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #endif
 }
 
+// test hook (artemis_debug_set_render_blocks): cap the persistent render
+// grid so a test can vary the ray-to-warp schedule; results must not change
+static int g_render_block_cap = 0;
+
 template <int kMode, int kRays, bool kVec, bool kDDA>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
@@ -913,7 +923,8 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         int occ = 0;                                                                            \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRenderThreads, smem);        \
-        const int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * (occ > 0 ? occ : 1)); \
+        int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * (occ > 0 ? occ : 1)); \
+        if (g_render_block_cap > 0 && blocks > g_render_block_cap) blocks = g_render_block_cap; \
         kern<<<blocks, kRenderThreads, smem, st>>>(a);                                          \
         break;                                                                                  \
     }
@@ -1025,6 +1036,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         const int stride = shade->coef_stride > 0 ? shade->coef_stride
                                                   : (shade->degree + 1) * (shade->degree + 1) * shade->channels;
         a.no_row_prefetch = flut_rows > 0 && (double)flut_rows * stride * 4.0 <= 0.5 * l2;
+        a.n_rows = flut_rows;
     }
     if (n_views > 1) {  // several views of one tree in one launch (unsharded, own outputs)
         if (n_views > kMaxViews || sharded || (peer_out && peer_out[0])) return ARTEMIS_ERR_ARG;
@@ -1211,6 +1223,12 @@ extern "C" int artemis_forward_fit(const artemis_tree_view *tree, const artemis_
         return launch_render_deg<kTrace, 0>(shade->degree, a,
                                                 ceil_div<int64_t>(rays->n_rays, 32), S(stream));
     });
+}
+
+extern "C" int artemis_debug_set_render_blocks(int max_blocks) {
+    if (max_blocks < 0) return ARTEMIS_ERR_ARG;
+    g_render_block_cap = max_blocks;
+    return ARTEMIS_OK;
 }
 
 extern "C" int artemis_camera_rays(const artemis_camera *cam, double *og, double *dg, double *dw,

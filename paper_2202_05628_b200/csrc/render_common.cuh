@@ -29,6 +29,7 @@ struct RenderArgs {
     const double *rot_inv;
     int channels;
     int coef_stride;
+    int64_t n_rows;  // FLUT rows (0 = unknown; debug checks only)
     // rays: explicit arrays or a camera (device pointer, read once)
     const double *og, *dg, *dw;
     const artemis_camera *cam;

@@ -119,11 +119,13 @@ __global__ void __launch_bounds__(kBlock) resolve_kernel(
             best_s = so;
         }
     }
+    ARTEMIS_DCHECK(u >= 0 && u < n && u <= i);
     if (rank == 0) {
         live_codes[u] = c;
         winners[u] = me;
     } else if (kPairs) {
         int64_t row = s - u + rank - 1;
+        ARTEMIS_DCHECK(row >= 0 && row < n);
         pairs[2 * row] = (int64_t)best;
         pairs[2 * row + 1] = (int64_t)me;
     }

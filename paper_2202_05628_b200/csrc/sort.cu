@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
         if (idx < n) {
             uint32_t dd = (uint32_t)((key[j] >> shift) & 0xFF);
             uint32_t lp = tpre[dd] + whist[warp][dd] + rank[j];
+            ARTEMIS_DCHECK(lp < (uint32_t)kTile);
             skey[lp] = key[j];
             sval[lp] = val[j];
         }
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     for (int i = tid; i < tile_n; i += kThreads) {
         const K k = skey[i];
         const uint32_t pos = dbase[(uint32_t)((k >> shift) & 0xFF)] + (uint32_t)i;
+        ARTEMIS_DCHECK((int64_t)pos < n);
         kout[pos] = k;
         vout[pos] = sval[i];
     }
