@@ -74,6 +74,45 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 
 
 
+#ifndef ARTEMIS_STREAM_OUT
+#define ARTEMIS_STREAM_OUT 0  // 1: output maps stored evict-first (st.global.cs)
+#endif
+#ifndef ARTEMIS_ROW_HINT
+#define ARTEMIS_ROW_HINT 0  // 1: FLUT row loads carry an L2 evict_last policy
+#endif
+
+// Output stores: with ARTEMIS_STREAM_OUT the maps bypass L2 residency
+// (streaming, evict-first) so they do not push FLUT rows out of L2.
+template <typename T>
+__device__ __forceinline__ void st_out(T *p, T v) {
+    if (ARTEMIS_STREAM_OUT)
+        __stcs(p, v);
+    else
+        *p = v;
+}
+
+__device__ __forceinline__ uint64_t row_policy() {
+    uint64_t pol = 0;
+#if ARTEMIS_ROW_HINT
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
+}
+
+// One 16-byte slice of a FLUT row (read-only path; optionally evict_last in L2).
+__device__ __forceinline__ float4 ld_row(const float4 *p, uint64_t pol) {
+#if ARTEMIS_ROW_HINT
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(p);
+#endif
+}
+
 // Ray/box overlap of the child box packed in (w0, w1, w2) within
 // [t_min, t_max]; exact port of the slab test (_core.pyx:252-285).
 __device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2,
@@ -225,6 +264,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.channels;
     const int cp = kVec ? C : (C | 1);
+    const uint64_t l2pol = row_policy();
     using FeatT = float;  // per-ray feature sums
     FeatT *feat = reinterpret_cast<FeatT *>(s_raw + kStackB + kQueueBytes) +
                   (size_t)warp * 32 * cp;
@@ -800,7 +840,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                         for (int c4 = q; c4 < units; c4 += lph) {
                             float4 v[H];
 #pragma unroll
-                            for (int h = 0; h < H; ++h) v[h] = __ldg(row + h * units + c4);
+                            for (int h = 0; h < H; ++h) v[h] = ld_row(row + h * units + c4, l2pol);
                             unsigned mm = members;
                             while (mm) {
                                 const int s = __ffs(mm) - 1;
@@ -861,18 +901,18 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             } else {
                 if (kMulti) {  // per-view maps
                     if (p.A64) {
-                        static_cast<double *>(p.Av[rv])[ray] = acc;
-                        static_cast<double *>(p.Dv[rv])[ray] = depth;
+                        st_out(static_cast<double *>(p.Av[rv]) + ray, acc);
+                        st_out(static_cast<double *>(p.Dv[rv]) + ray, depth);
                     } else {
-                        static_cast<float *>(p.Av[rv])[ray] = (float)acc;
-                        static_cast<float *>(p.Dv[rv])[ray] = (float)depth;
+                        st_out(static_cast<float *>(p.Av[rv]) + ray, (float)acc);
+                        st_out(static_cast<float *>(p.Dv[rv]) + ray, (float)depth);
                     }
                 } else {
-                    if (p.A64) p.A64[ray] = acc;
-                    if (p.A32) p.A32[ray] = (float)acc;
+                    if (p.A64) st_out(p.A64 + ray, acc);
+                    if (p.A32) st_out(p.A32 + ray, (float)acc);
                     if (kMode == kRender) {
-                        if (p.D64) p.D64[ray] = depth;
-                        if (p.D32) p.D32[ray] = (float)depth;
+                        if (p.D64) st_out(p.D64 + ray, depth);
+                        if (p.D32) st_out(p.D32 + ray, (float)depth);
                     }
                 }
             }
@@ -887,7 +927,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 float *Fo = p.F;
                 if (kMulti) Fo = p.Fv[__shfl_sync(0xffffffffu, rv, s)];
                 for (int c = lane; c < C; c += 32) {
-                    Fo[r * C + c] = feat[s * cp + c];
+                    st_out(Fo + r * C + c, feat[s * cp + c]);
                     feat[s * cp + c] = FeatT(0);
                 }
             }

@@ -25,6 +25,9 @@ for a in sys.argv[1:]:
     if a.startswith("--steps="):
         steps = int(a.split("=")[1])
 names = args or ["c0", "c1", "c2", "c3", "c4"]
+if os.environ.get("ARTEMIS_RENDER_BLOCKS"):  # experiment: cap the persistent render grid
+    from paper_2202_05628_b200 import _lib  # noqa: E402
+    _lib.lib().artemis_debug_set_render_blocks(int(os.environ["ARTEMIS_RENDER_BLOCKS"]))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 for name in names:

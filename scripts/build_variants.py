@@ -8,6 +8,10 @@ from paper_2202_05628_b200 import build_lib  # noqa: E402
 VARIANTS = {
     "base": (),
     "checks": ("ARTEMIS_DEBUG_CHECKS=1",),
+    "sout": ("ARTEMIS_STREAM_OUT=1",),
+    "rhint": ("ARTEMIS_ROW_HINT=1",),
+    "sout_rhint": ("ARTEMIS_STREAM_OUT=1", "ARTEMIS_ROW_HINT=1"),
+    "sout_nopf": ("ARTEMIS_STREAM_OUT=1", "ARTEMIS_ROW_PREFETCH=0"),
     "clocks": ("ARTEMIS_PHASE_CLOCKS=1",),
     "nodedup": ("ARTEMIS_DEDUP=0",),
     "q8t96": ("ARTEMIS_QCAP=8", "ARTEMIS_QTHRESH=96", "ARTEMIS_MIN_BLOCKS=3"),
