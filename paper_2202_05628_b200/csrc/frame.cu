@@ -37,7 +37,12 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
                   const double *w, const double *aff, int n_joints, const double lo[3],
                   const double cell[3], int res, int key_bytes, void *keys, uint32_t *vals,
                   int32_t *rot_joint, int32_t *n_in, uint64_t sentinel, int identity,
-                  cudaStream_t st);
+                  uint32_t *bmask, uint32_t *bocc, cudaStream_t st);
+int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const double *sigma,
+                     uint32_t *bocc, uint32_t *bmask, int64_t n_words, uint32_t *wtmp,
+                     BrickRec *recs, int32_t *table, const int dims[3], int32_t *aabb,
+                     uint32_t *live_codes, uint32_t *winners, unsigned long long *wkey,
+                     int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
@@ -87,6 +92,13 @@ struct artemis_frame_s {
     BrickRec *brecs = nullptr;
     int bdims[3] = {1, 1, 1};
     artemis_brickmap bmap{};
+    // counting rebuild (rebuild.cu) for grids <= 1024^3: dense per-brick cell
+    // masks + brick bitmap (both kept zero between frames), per-word counts,
+    // per-live-cell density keys
+    int counting = 0;
+    uint32_t *bmask = nullptr, *bocc = nullptr, *wtmp = nullptr;
+    int64_t n_words = 0;
+    unsigned long long *wkey = nullptr;
     void *sort_ws = nullptr, *resolve_ws = nullptr;
     size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
     FrameParams *params = nullptr;
@@ -240,10 +252,31 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     }
     rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,
                        identity ? 1 : n_joints, f->lo, f->cell, as.resolution, f->key_bytes,
-                       f->keys, f->vals, f->rot_joint, f->counters, f->sentinel, identity, st);
+                       f->keys, f->vals, f->rot_joint, f->counters, f->sentinel, identity,
+                       f->counting ? f->bmask : nullptr, f->counting ? f->bocc : nullptr, st);
     if (rc) return rc;
     launches += 1;
     mark(1);
+    if (f->counting) {
+        // counting rebuild: Morton order and collision winners without a
+        // sort (rebuild.cu), the brick map in the same passes
+        rc = counting_rebuild((const uint32_t *)f->keys, f->n, (uint32_t)f->sentinel, as.sigma,
+                              f->bocc, f->bmask, f->n_words, f->wtmp, f->brecs, f->btable,
+                              f->bdims, f->bmeta + 1, (uint32_t *)f->live_codes, f->winners,
+                              f->wkey, f->counters + 1, f->bmeta, st, &launches);
+        if (rc) return rc;
+        mark(2);
+        mark(3);
+        rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
+                                         f->n, f->left, f->right, f->bmin, f->bsize, nullptr,
+                                         f->leaves, f->winners, as.sigma, f->rot_joint, nullptr,
+                                         st);
+        if (rc) return rc;
+        launches += 1;  // the Karras build (count/scan/emit/slot/winner counted above)
+        // the side stream only cleared the outputs: join it before the render
+        ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));
+        ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
+    } else {
     // the Karras tree arrays (reference layout) are rebuilt every frame: they
     // are the rebuild stage's output (volume.build_octree) even though the
     // renderer walks the brick map
@@ -286,9 +319,10 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     if (rc) return rc;
     ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
     launches += 2;  // the brick passes (side stream)
-    mark(4);
     const int passes = f->key_bits <= 0 ? 1 : (f->key_bits + 7) / 8;
     launches += 2 + passes + 3 + 1;  // + 2 brick passes counted above
+    }
+    mark(4);
     artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution, &f->bmap};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
@@ -501,6 +535,22 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
     rc = rc ? rc : dev_alloc(&f->btable, (size_t)f->bdims[0] * f->bdims[1] * f->bdims[2] * 4);
     rc = rc ? rc : dev_alloc(&f->brecs, (size_t)(n + 1) * sizeof(BrickRec));
     rc = rc ? rc : dev_alloc(&f->bmeta, 64);
+    {   // counting rebuild for 32-bit keys (grids <= 1024^3); ARTEMIS_COUNTING=0
+        // selects the onesweep sort + resolve path instead (A/B, tests)
+        const char *env = getenv("ARTEMIS_COUNTING");
+        f->counting = f->key_bytes == 4 && a->resolution <= 1024 && !(env && env[0] == '0');
+    }
+    if (!rc && f->counting) {
+        const int64_t bricks = (int64_t)f->bdims[0] * f->bdims[1] * f->bdims[2];
+        f->n_words = (bricks + 31) / 32;
+        rc = rc ? rc : dev_alloc(&f->bmask, (size_t)f->n_words * 32 * 16 * 4);
+        rc = rc ? rc : dev_alloc(&f->bocc, (size_t)f->n_words * 4);
+        rc = rc ? rc : dev_alloc(&f->wtmp, (size_t)f->n_words * 8);
+        rc = rc ? rc : dev_alloc(&f->wkey, (size_t)n * 8);
+        if (!rc && (cudaMemset(f->bmask, 0, (size_t)f->n_words * 32 * 16 * 4) != cudaSuccess ||
+                    cudaMemset(f->bocc, 0, (size_t)f->n_words * 4) != cudaSuccess))
+            rc = ARTEMIS_ERR_CUDA;
+    }
     if (!rc) {
         f->bmap.table = f->btable;
         f->bmap.recs = f->brecs;
@@ -551,7 +601,7 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
                     f->leaves, f->btable, f->brecs, f->bmeta,
-                    f->sort_ws, f->resolve_ws, f->params};
+                    f->sort_ws, f->resolve_ws, f->params, f->bmask, f->bocc, f->wtmp, f->wkey};
     for (void *b : bufs)
         if (b) cudaFree(b);
     delete f;

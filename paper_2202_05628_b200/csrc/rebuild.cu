@@ -1,0 +1,274 @@
+// Counting rebuild of the posed leaf set (frame pipeline, grids <= 1024^3).
+//
+// Replaces, for the device frame, the reference's stable radix sort of the
+// warped Morton keys (volume.build_octree -> sort_order, _core.pyx:111-167)
+// and its collision resolve (rigging.resolve_collisions, rigging.py:419-459:
+// np.lexsort((idx, -sigma, code)), the first entry of each code wins). The
+// output is the same: the live codes strictly ascending, each with its
+// winner (largest density, ties to the lowest canonical index, NaN
+// densities last) -- plus the occupancy brick map the renderer walks.
+//
+// A Morton code is (brick code << 9) | (cell code within the 8^3 brick), so
+// ascending codes are bricks in Morton order and, inside a brick, the
+// 512-bit occupancy mask in bit order. The sort is therefore a two-digit
+// counting sort over the key space instead of four 8-bit scatter passes:
+//   warp kernel   sets the cell's bit in a dense per-brick mask and the
+//                 brick's bit in a brick-occupancy bitmap (warp-aggregated
+//                 atomicOr: order-independent)
+//   count         per bitmap word: occupied bricks, live cells (popcounts)
+//   scan          exclusive scans of both (one block)
+//   emit          per occupied brick, in Morton order: its record (mask,
+//                 per-word prefix, first leaf), the dense brick table entry,
+//                 the leaf-cell AABB; clears the dense masks for the next frame
+//   slot          per in-bounds voxel: its live-cell rank = record.first +
+//                 prefix + popc(mask below the bit); live code; atomicMax of
+//                 the density's total-order key
+//   winner        per in-bounds voxel holding the maximal key: atomicMin of
+//                 its canonical index -> the winner
+// Integer atomics (or / max / min) commute, so the result is deterministic
+// and equals the reference's order, with no per-entry sort at all.
+#include "bricks.cuh"
+#include "tree.cuh"
+
+namespace artemis {
+
+namespace {
+constexpr int kCountThreads = 256;
+}
+
+// Density total order of the reference's lexsort on -sigma: larger first,
+// -0.0 == +0.0, NaN after every number (key 0).
+__device__ __forceinline__ unsigned long long density_key(double s) {
+    if (isnan(s)) return 0ull;
+    if (s == 0.0) s = 0.0;  // -0.0 ties with +0.0, as in the lexsort
+    const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// live cells of brick b (popcount of its 512-bit mask)
+__device__ __forceinline__ uint32_t brick_cells(const uint32_t *__restrict__ bmask, u64 b) {
+    const uint4 *m = reinterpret_cast<const uint4 *>(bmask + b * 16);
+    uint32_t cells = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 v = m[q];
+        cells += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    }
+    return cells;
+}
+
+// one warp per bitmap word (lane j = brick 32 w + j): occupied bricks and
+// live cells of the word
+__global__ void count_kernel(const uint32_t *__restrict__ bocc,
+                             const uint32_t *__restrict__ bmask, int64_t n_words,
+                             uint32_t *__restrict__ n_bricks, uint32_t *__restrict__ n_cells) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= n_words) return;
+    const uint32_t occ = bocc[w];
+    const uint32_t c = ((occ >> lane) & 1u) ? brick_cells(bmask, (u64)(32 * w + lane)) : 0u;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) {
+        n_bricks[w] = __popc(occ);
+        n_cells[w] = tot;
+    }
+}
+
+// exclusive scans of both count arrays (one block), totals to n_live / n_recs
+__global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, int64_t n,
+                                                     int32_t *total_b, int32_t *total_a) {
+    __shared__ uint32_t sa[32], sb[32];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t lo = t * per, hi = min(n, lo + per);
+    uint32_t xa = 0, xb = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+        xa += a[i];
+        xb += b[i];
+    }
+    uint32_t ia = xa, ib = xb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o);
+        const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) {
+            ia += ya;
+            ib += yb;
+        }
+    }
+    if (lane == 31) {
+        sa[wid] = ia;
+        sb[wid] = ib;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t va = sa[lane], vb = sb[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(0xffffffffu, va, o);
+            const uint32_t yb = __shfl_up_sync(0xffffffffu, vb, o);
+            if (lane >= o) {
+                va += ya;
+                vb += yb;
+            }
+        }
+        sa[lane] = va;
+        sb[lane] = vb;
+    }
+    __syncthreads();
+    uint32_t ea = (wid ? sa[wid - 1] : 0u) + ia - xa;
+    uint32_t eb = (wid ? sb[wid - 1] : 0u) + ib - xb;
+    for (int64_t i = lo; i < hi; ++i) {
+        const uint32_t va = a[i], vb = b[i];
+        a[i] = ea;
+        b[i] = eb;
+        ea += va;
+        eb += vb;
+    }
+    if (t == 1023) {
+        *total_a = (int32_t)ea;
+        *total_b = (int32_t)eb;
+    }
+}
+
+// one warp per bitmap word (lane j = brick 32 w + j): each occupied brick's
+// record, table entry and live slots (initialised for slot/winner), the
+// leaf-cell AABB; clears the dense masks and the bitmap word for the next frame
+__global__ void emit_kernel(uint32_t *__restrict__ bocc, uint32_t *__restrict__ bmask,
+                            int64_t n_words, const uint32_t *__restrict__ rec_base,
+                            const uint32_t *__restrict__ cell_base, BrickRec *__restrict__ recs,
+                            int32_t *__restrict__ table, int dx, int dy,
+                            unsigned long long *__restrict__ wkey,
+                            uint32_t *__restrict__ widx, int32_t *aabb) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    const uint32_t occ = w < n_words ? bocc[w] : 0u;
+    const bool mine = (occ >> lane) & 1u;
+    const u64 b = (u64)(32 * w + lane);
+    const uint32_t cnt = mine ? brick_cells(bmask, b) : 0u;
+    uint32_t incl = cnt;  // warp inclusive scan of the cell counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (mine) {
+        const uint32_t rec = rec_base[w] + __popc(occ & ((1u << lane) - 1u));
+        const uint32_t first = cell_base[w] + incl - cnt;
+        uint32_t *mk = bmask + b * 16;
+        BrickRec &R = recs[rec];
+        const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
+                  bz = (int)compact_bits3(b >> 2);
+        uint32_t run = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const uint32_t m = mk[q];
+            R.mask[q] = m;
+            R.prefix[q] = (uint16_t)run;
+            uint32_t mm = m;
+            while (mm) {  // exact leaf-cell AABB from the occupied bits
+                const int bit = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const u64 l = (u64)(q * 32 + bit);
+                const int c[3] = {bx * 8 + (int)compact_bits3(l), by * 8 + (int)compact_bits3(l >> 1),
+                                  bz * 8 + (int)compact_bits3(l >> 2)};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    lo[a] = min(lo[a], c[a]);
+                    hi[a] = max(hi[a], c[a] + 1);
+                }
+            }
+            run += __popc(m);
+            mk[q] = 0u;  // ready for the next frame
+        }
+        R.first = first;
+        for (uint32_t k = 0; k < run; ++k) {  // the brick's live slots
+            wkey[first + k] = 0ull;
+            widx[first + k] = 0xFFFFFFFFu;
+        }
+        table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
+    }
+    if (w < n_words && lane == 0) bocc[w] = 0u;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+    }
+    if (lane == 0 && lo[0] != INT32_MAX) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(aabb + a, lo[a]);
+            atomicMax(aabb + 3 + a, hi[a]);
+        }
+    }
+}
+
+// live-cell rank of an in-bounds voxel's key (from its brick record)
+__device__ __forceinline__ uint32_t live_rank(uint32_t key, const int32_t *__restrict__ table,
+                                              const BrickRec *__restrict__ recs, int dx,
+                                              int dy) {
+    const u64 b = (u64)(key >> 9);
+    const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
+              bz = (int)compact_bits3(b >> 2);
+    const BrickRec &R = recs[table[((size_t)bz * dy + by) * dx + bx]];
+    const uint32_t l = key & 511u, q = l >> 5;
+    return R.first + R.prefix[q] + (uint32_t)__popc(R.mask[q] & ((1u << (l & 31u)) - 1u));
+}
+
+__global__ void slot_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32_t sentinel,
+                            const double *__restrict__ sigma, const int32_t *__restrict__ table,
+                            const BrickRec *__restrict__ recs, int dx, int dy,
+                            uint32_t *__restrict__ live_codes,
+                            unsigned long long *__restrict__ wkey) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t key = keys[i];
+    if (key == sentinel) return;
+    const uint32_t s = live_rank(key, table, recs, dx, dy);
+    live_codes[s] = key;  // every voxel of the cell writes the same code
+    atomicMax(wkey + s, density_key(sigma[i]));
+}
+
+__global__ void winner_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32_t sentinel,
+                              const double *__restrict__ sigma,
+                              const int32_t *__restrict__ table,
+                              const BrickRec *__restrict__ recs, int dx, int dy,
+                              const unsigned long long *__restrict__ wkey,
+                              uint32_t *__restrict__ widx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t key = keys[i];
+    if (key == sentinel) return;
+    const uint32_t s = live_rank(key, table, recs, dx, dy);
+    if (density_key(sigma[i]) == wkey[s]) atomicMin(widx + s, (uint32_t)i);
+}
+
+// The counting rebuild after the warp kernel marked bmask / bocc: leaves
+// (codes ascending, winners) + brick map. keys are indexed by canonical voxel
+// (sentinel = out of bounds); n_live / n_recs receive the counts.
+int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const double *sigma,
+                     uint32_t *bocc, uint32_t *bmask, int64_t n_words, uint32_t *wtmp,
+                     BrickRec *recs, int32_t *table, const int dims[3], int32_t *aabb,
+                     uint32_t *live_codes, uint32_t *winners, unsigned long long *wkey,
+                     int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches) {
+    uint32_t *nb = wtmp, *nc = wtmp + n_words;
+    const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
+    ARTEMIS_TRY(cudaMemsetAsync(table, 0xFF, cells * sizeof(int32_t), st));
+    ARTEMIS_TRY(cudaMemsetAsync(aabb, 0x7F, 3 * sizeof(int32_t), st));
+    ARTEMIS_TRY(cudaMemsetAsync(aabb + 3, 0x80, 3 * sizeof(int32_t), st));
+    const int wb = (int)ceil_div<int64_t>(n_words * 32, kCountThreads);
+    count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc);
+    scan2_kernel<<<1, 1024, 0, st>>>(nc, nb, n_words, n_recs, n_live);
+    emit_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, recs, table, dims[0],
+                                              dims[1], wkey, winners, aabb);
+    const int vb = (int)ceil_div<int64_t>(n, kCountThreads);
+    slot_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
+                                              dims[1], live_codes, wkey);
+    winner_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
+                                                dims[1], wkey, winners);
+    if (launches) *launches += 5;
+    return ARTEMIS_LAUNCHED();
+}
+
+}  // namespace artemis

@@ -43,6 +43,10 @@ struct WarpArgs {
     int32_t *n_in;        // in-bounds counter
     uint64_t sentinel;
     int identity;         // 1 = no warp: canonical cells, rotation joint 0
+    // counting rebuild (rebuild.cu; 32-bit keys): dense per-brick cell masks
+    // and the brick-occupancy bitmap, both indexed by Morton code
+    uint32_t *bmask;
+    uint32_t *bocc;
 };
 
 template <typename K, bool kPipeline>
@@ -126,6 +130,22 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
     if (kPipeline) {
         unsigned b = __ballot_sync(0xffffffffu, live && ok);
         if ((threadIdx.x & 31) == 0 && b) atomicAdd(a.n_in, __popc(b));
+        if (sizeof(K) == 4 && a.bmask) {
+            // mark the cell in its brick mask (word = key >> 5) and the brick
+            // in the bitmap (word = key >> 14), one atomicOr per distinct word
+            // per warp (lanes hold neighbouring canonical voxels)
+            const bool on = live && ok;
+            const uint32_t key = on ? (uint32_t)morton3((u64)g[0], (u64)g[1], (u64)g[2]) : 0u;
+            const int lane = threadIdx.x & 31;
+            const uint32_t mw = on ? key >> 5 : 0xFFFFFFFFu;
+            const unsigned g1 = __match_any_sync(0xffffffffu, mw);
+            const uint32_t m1 = __reduce_or_sync(g1, on ? 1u << (key & 31u) : 0u);
+            if (on && lane == __ffs(g1) - 1) atomicOr(a.bmask + mw, m1);
+            const uint32_t bw = on ? key >> 14 : 0xFFFFFFFFu;
+            const unsigned g2 = __match_any_sync(0xffffffffu, bw);
+            const uint32_t m2 = __reduce_or_sync(g2, on ? 1u << ((key >> 9) & 31u) : 0u);
+            if (on && lane == __ffs(g2) - 1) atomicOr(a.bocc + bw, m2);
+        }
     }
 }
 
@@ -145,7 +165,7 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
                   const double *w, const double *aff, int n_joints, const double lo[3],
                   const double cell[3], int res, int key_bytes, void *keys, uint32_t *vals,
                   int32_t *rot_joint, int32_t *n_in, uint64_t sentinel, int identity,
-                  cudaStream_t st) {
+                  uint32_t *bmask, uint32_t *bocc, cudaStream_t st) {
     if (n_joints > kMaxJoints) return ARTEMIS_ERR_ARG;
     WarpArgs a{};
     a.cells = cells;
@@ -166,6 +186,8 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
     a.n_in = n_in;
     a.sentinel = sentinel;
     a.identity = identity;
+    a.bmask = bmask;
+    a.bocc = bocc;
     return key_bytes == 4 ? launch_warp<uint32_t>(a, true, st) : launch_warp<u64>(a, true, st);
 }
 
