@@ -77,6 +77,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_STREAM_OUT
 #define ARTEMIS_STREAM_OUT 0  // 1: output maps stored evict-first (st.global.cs)
 #endif
+#ifndef ARTEMIS_FLAT_SHADE
+#define ARTEMIS_FLAT_SHADE 0  // 1: shade a flat member list per level (see phase C)
+#endif
 #ifndef ARTEMIS_ROW_HINT
 #define ARTEMIS_ROW_HINT 0  // 1: FLUT row loads carry an L2 evict_last policy
 #endif
@@ -818,6 +821,59 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 (void)key;
 #endif
                 const bool leader = vis && lane == __ffs(grpm) - 1;
+#if ARTEMIS_FLAT_SHADE
+                if (kVec) {
+                    // flat member list: the level's visible lanes, groups of one FLUT
+                    // row adjacent (leader-lane order), so every lane group shades a
+                    // member each pass (no idle groups waiting on a long member
+                    // list); members of one row in the same pass load the same
+                    // addresses (one L1 request), later passes hit L1
+                    const int nvis = __popc(__ballot_sync(0xffffffffu, vis));
+                    const int x = leader ? __popc(grpm) : 0;
+                    int incl = x;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int goff = __shfl_sync(0xffffffffu, incl - x, __ffs(grpm) - 1);
+                    if (vis) wl[goff + __popc(grpm & lt)] = (uint16_t)lane;
+                    __syncwarp();
+                    for (int m = grp; m - grp < nvis; m += hpi) {
+                        if (m >= nvis) continue;
+                        const int s = (int)wl[m];
+                        const uint32_t bf = q_id[k * kRenderThreads + wbase + s] & ~kDenseFlag;
+                        const float4 *row =
+                            reinterpret_cast<const float4 *>(p.coef + (size_t)bf * p.coef_stride);
+                        const float4 bv = q_val[k * kRenderThreads + wbase + s];
+                        float Y[H];
+                        sh_basis_f<kDeg>(bv.y, bv.z, bv.w, Y);
+                        for (int c4 = q; c4 < units; c4 += lph) {
+                            float4 v[H];
+#pragma unroll
+                            for (int h = 0; h < H; ++h) v[h] = ld_row(row + h * units + c4, l2pol);
+                            float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f;
+#pragma unroll
+                            for (int h = 0; h < H; ++h) {
+                                ax = fmaf(v[h].x, Y[h], ax);
+                                ay = fmaf(v[h].y, Y[h], ay);
+                                az = fmaf(v[h].z, Y[h], az);
+                                aw = fmaf(v[h].w, Y[h], aw);
+                            }
+                            float4 *dst =
+                                reinterpret_cast<float4 *>(reinterpret_cast<float *>(feat) + s * cp) + c4;
+                            float4 f = *dst;
+                            f.x += bv.x * ax;
+                            f.y += bv.x * ay;
+                            f.z += bv.x * az;
+                            f.w += bv.x * aw;
+                            *dst = f;
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+                }
+#endif
                 const unsigned ml = __ballot_sync(0xffffffffu, leader);
                 const int cnt = __popc(ml);
 #ifdef ARTEMIS_PHASE_CLOCKS
