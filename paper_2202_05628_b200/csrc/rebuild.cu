@@ -27,6 +27,8 @@
 //                 its canonical index -> the winner
 // Integer atomics (or / max / min) commute, so the result is deterministic
 // and equals the reference's order, with no per-entry sort at all.
+#include <algorithm>
+
 #include "bricks.cuh"
 #include "tree.cuh"
 
@@ -57,20 +59,99 @@ __device__ __forceinline__ uint32_t brick_cells(const uint32_t *__restrict__ bma
     return cells;
 }
 
-// one warp per bitmap word (lane j = brick 32 w + j): occupied bricks and
-// live cells of the word
+// exact leaf-cell AABB of the cells in mask word q (local Morton index
+// l = 32 q + i: x = l0 + 2 l3 + 4 l6, y = l1 + 2 l4 + 4 l7, z = l2 + 2 l5 +
+// 4 l8, l5..l8 = bits of q) from bit patterns, no loop over the bits
+__device__ __forceinline__ void word_aabb(uint32_t m, int q, int bx, int by, int bz, int lo[3],
+                                          int hi[3]) {
+    if (!m) return;
+    const uint32_t X[4] = {0x550055u, 0xaa00aau, 0x55005500u, 0xaa00aa00u};
+    const uint32_t Y[4] = {0x3333u, 0xccccu, 0x33330000u, 0xcccc0000u};
+    int xl = 3, xh = 0, yl = 3, yh = 0;
+#pragma unroll
+    for (int v = 3; v >= 0; --v) {
+        if (m & X[v]) xl = v;
+        if (m & Y[v]) yl = v;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        if (m & X[v]) xh = v;
+        if (m & Y[v]) yh = v;
+    }
+    const int zl = (m & 0x0f0f0f0fu) ? 0 : 1, zh = (m & 0xf0f0f0f0u) ? 1 : 0;
+    const int xo = bx * 8 + 4 * ((q >> 1) & 1), yo = by * 8 + 4 * ((q >> 2) & 1),
+              zo = bz * 8 + 2 * (q & 1) + 4 * ((q >> 3) & 1);
+    lo[0] = min(lo[0], xo + xl);
+    hi[0] = max(hi[0], xo + xh + 1);
+    lo[1] = min(lo[1], yo + yl);
+    hi[1] = max(hi[1], yo + yh + 1);
+    lo[2] = min(lo[2], zo + zl);
+    hi[2] = max(hi[2], zo + zh + 1);
+}
+
+// one warp per bitmap word (lane j = brick 32 w + j): the word's occupied
+// bricks and live cells, each brick's cell offset within the word, and the
+// exact leaf-cell AABB (block-reduced, then one atomic per bound and block)
 __global__ void count_kernel(const uint32_t *__restrict__ bocc,
                              const uint32_t *__restrict__ bmask, int64_t n_words,
-                             uint32_t *__restrict__ n_bricks, uint32_t *__restrict__ n_cells) {
+                             uint32_t *__restrict__ n_bricks, uint32_t *__restrict__ n_cells,
+                             uint32_t *__restrict__ bpre, int32_t *aabb) {
+    __shared__ int red[6][kCountThreads / 32];
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= n_words) return;
-    const uint32_t occ = bocc[w];
-    const uint32_t c = ((occ >> lane) & 1u) ? brick_cells(bmask, (u64)(32 * w + lane)) : 0u;
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
-    if (lane == 0) {
-        n_bricks[w] = __popc(occ);
-        n_cells[w] = tot;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    const uint32_t occ = w < n_words ? bocc[w] : 0u;
+    uint32_t c = 0;
+    if ((occ >> lane) & 1u) {
+        const u64 b = (u64)(32 * w + lane);
+        const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
+                  bz = (int)compact_bits3(b >> 2);
+        const uint4 *m4 = reinterpret_cast<const uint4 *>(bmask + b * 16);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 v = m4[q4];
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            word_aabb(v.x, 4 * q4, bx, by, bz, lo, hi);
+            word_aabb(v.y, 4 * q4 + 1, bx, by, bz, lo, hi);
+            word_aabb(v.z, 4 * q4 + 2, bx, by, bz, lo, hi);
+            word_aabb(v.w, 4 * q4 + 3, bx, by, bz, lo, hi);
+        }
+    }
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (w < n_words) {
+        bpre[32 * w + lane] = incl - c;
+        if (lane == 31) {
+            n_bricks[w] = __popc(occ);
+            n_cells[w] = incl;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            red[a][wid] = lo[a];
+            red[3 + a][wid] = hi[a];
+        }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        int r = red[k][0];
+        for (int v = 1; v < kCountThreads / 32; ++v) r = k < 3 ? min(r, red[k][v]) : max(r, red[k][v]);
+        if (k < 3 ? r != INT32_MAX : r != INT32_MIN) {
+            if (k < 3)
+                atomicMin(aabb + k, r);
+            else
+                atomicMax(aabb + k, r);
+        }
     }
 }
 
@@ -82,7 +163,8 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     const int64_t per = (n + 1023) / 1024;
     const int64_t lo = t * per, hi = min(n, lo + per);
     uint32_t xa = 0, xb = 0;
-    for (int64_t i = lo; i < hi; ++i) {
+#pragma unroll 8
+    for (int64_t i = lo; i < hi; ++i) {  // unrolled: the loads of a batch overlap
         xa += a[i];
         xb += b[i];
     }
@@ -118,6 +200,7 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     __syncthreads();
     uint32_t ea = (wid ? sa[wid - 1] : 0u) + ia - xa;
     uint32_t eb = (wid ? sb[wid - 1] : 0u) + ib - xb;
+#pragma unroll 8
     for (int64_t i = lo; i < hi; ++i) {
         const uint32_t va = a[i], vb = b[i];
         a[i] = ea;
@@ -131,76 +214,50 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     }
 }
 
-// one warp per bitmap word (lane j = brick 32 w + j): each occupied brick's
-// record, table entry and live slots (initialised for slot/winner), the
-// leaf-cell AABB; clears the dense masks and the bitmap word for the next frame
-__global__ void emit_kernel(uint32_t *__restrict__ bocc, uint32_t *__restrict__ bmask,
-                            int64_t n_words, const uint32_t *__restrict__ rec_base,
-                            const uint32_t *__restrict__ cell_base, BrickRec *__restrict__ recs,
+// one warp per brick (most exit at once: unoccupied): an occupied brick's
+// record (mask, per-word prefix, first leaf), its table entry and its live
+// slots (initialised for slot/winner, coalesced); clears its dense mask for
+// the next frame
+__global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restrict__ bmask,
+                            int64_t n_bricks_dense, const uint32_t *__restrict__ rec_base,
+                            const uint32_t *__restrict__ cell_base,
+                            const uint32_t *__restrict__ bpre, BrickRec *__restrict__ recs,
                             int32_t *__restrict__ table, int dx, int dy,
                             unsigned long long *__restrict__ wkey,
-                            uint32_t *__restrict__ widx, int32_t *aabb) {
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                            uint32_t *__restrict__ widx) {
+    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
-    const uint32_t occ = w < n_words ? bocc[w] : 0u;
-    const bool mine = (occ >> lane) & 1u;
-    const u64 b = (u64)(32 * w + lane);
-    const uint32_t cnt = mine ? brick_cells(bmask, b) : 0u;
-    uint32_t incl = cnt;  // warp inclusive scan of the cell counts
+    if (b >= n_bricks_dense) return;
+    const int64_t w = b >> 5;
+    const int j = (int)(b & 31);
+    const uint32_t occ = bocc[w];
+    if (!((occ >> j) & 1u)) return;  // warp-uniform
+    const uint32_t rec = rec_base[w] + __popc(occ & ((1u << j) - 1u));
+    const uint32_t first = cell_base[w] + bpre[b];
+    uint32_t *mk = bmask + b * 16;
+    BrickRec &R = recs[rec];
+    const uint32_t m = lane < 16 ? mk[lane] : 0u;
+    uint32_t pre = __popc(m);  // inclusive scan of the word popcounts
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+    for (int o = 1; o < 16; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += y;
     }
-    if (mine) {
-        const uint32_t rec = rec_base[w] + __popc(occ & ((1u << lane) - 1u));
-        const uint32_t first = cell_base[w] + incl - cnt;
-        uint32_t *mk = bmask + b * 16;
-        BrickRec &R = recs[rec];
-        const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
-                  bz = (int)compact_bits3(b >> 2);
-        uint32_t run = 0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const uint32_t m = mk[q];
-            R.mask[q] = m;
-            R.prefix[q] = (uint16_t)run;
-            uint32_t mm = m;
-            while (mm) {  // exact leaf-cell AABB from the occupied bits
-                const int bit = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const u64 l = (u64)(q * 32 + bit);
-                const int c[3] = {bx * 8 + (int)compact_bits3(l), by * 8 + (int)compact_bits3(l >> 1),
-                                  bz * 8 + (int)compact_bits3(l >> 2)};
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    lo[a] = min(lo[a], c[a]);
-                    hi[a] = max(hi[a], c[a] + 1);
-                }
-            }
-            run += __popc(m);
-            mk[q] = 0u;  // ready for the next frame
-        }
+    const uint32_t run = __shfl_sync(0xffffffffu, pre, 15);
+    if (lane < 16) {
+        R.mask[lane] = m;
+        R.prefix[lane] = (uint16_t)(pre - __popc(m));
+        mk[lane] = 0u;  // ready for the next frame
+    }
+    if (lane == 0) {
         R.first = first;
-        for (uint32_t k = 0; k < run; ++k) {  // the brick's live slots
-            wkey[first + k] = 0ull;
-            widx[first + k] = 0xFFFFFFFFu;
-        }
+        const int bx = (int)compact_bits3((u64)b), by = (int)compact_bits3((u64)b >> 1),
+                  bz = (int)compact_bits3((u64)b >> 2);
         table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
     }
-    if (w < n_words && lane == 0) bocc[w] = 0u;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
-        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
-    }
-    if (lane == 0 && lo[0] != INT32_MAX) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            atomicMin(aabb + a, lo[a]);
-            atomicMax(aabb + 3 + a, hi[a]);
-        }
+    for (uint32_t k = lane; k < run; k += 32) {  // the brick's live slots
+        wkey[first + k] = 0ull;
+        widx[first + k] = 0xFFFFFFFFu;
     }
 }
 
@@ -220,8 +277,10 @@ __global__ void slot_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32
                             const double *__restrict__ sigma, const int32_t *__restrict__ table,
                             const BrickRec *__restrict__ recs, int dx, int dy,
                             uint32_t *__restrict__ live_codes,
-                            unsigned long long *__restrict__ wkey) {
+                            unsigned long long *__restrict__ wkey, uint32_t *__restrict__ bocc,
+                            int64_t n_words) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n_words) bocc[i] = 0u;  // emit has read the bitmap: clear it for the next frame
     if (i >= n) return;
     const uint32_t key = keys[i];
     if (key == sentinel) return;
@@ -258,15 +317,17 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
     ARTEMIS_TRY(cudaMemsetAsync(aabb, 0x7F, 3 * sizeof(int32_t), st));
     ARTEMIS_TRY(cudaMemsetAsync(aabb + 3, 0x80, 3 * sizeof(int32_t), st));
     const int wb = (int)ceil_div<int64_t>(n_words * 32, kCountThreads);
-    count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc);
+    uint32_t *bpre = wtmp + 2 * n_words;  // per dense brick: cells before it in its word
+    count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bpre, aabb);
     scan2_kernel<<<1, 1024, 0, st>>>(nc, nb, n_words, n_recs, n_live);
-    emit_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, recs, table, dims[0],
-                                              dims[1], wkey, winners, aabb);
-    const int vb = (int)ceil_div<int64_t>(n, kCountThreads);
+    const int64_t n_bricks = n_words * 32;
+    emit_kernel<<<(int)ceil_div<int64_t>(n_bricks * 32, kCountThreads), kCountThreads, 0, st>>>(
+        bocc, bmask, n_bricks, nb, nc, bpre, recs, table, dims[0], dims[1], wkey, winners);
+    const int vb = (int)ceil_div<int64_t>(std::max<int64_t>(n, n_words), kCountThreads);
     slot_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
-                                              dims[1], live_codes, wkey);
-    winner_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
-                                                dims[1], wkey, winners);
+                                              dims[1], live_codes, wkey, bocc, n_words);
+    winner_kernel<<<(int)ceil_div<int64_t>(n, kCountThreads), kCountThreads, 0, st>>>(
+        keys, n, sentinel, sigma, table, recs, dims[0], dims[1], wkey, winners);
     if (launches) *launches += 5;
     return ARTEMIS_LAUNCHED();
 }

@@ -331,7 +331,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // exact cell walk state (kDDA): current cell, step signs, exact entry /
     // exit crossing per axis, the leaf AABB exit, the cached brick
     int cc[3] = {0, 0, 0}, cs[3] = {0, 0, 0};
-    double cE[3] = {0, 0, 0}, cX[3] = {0, 0, 0};
+    // cell entry = max over the axes' slab entry crossings; it is the crossing
+    // of the last step (steps are time-ordered, a synced slab's entry is never
+    // later than the sync time), so one scalar replaces the per-axis entries
+    double t_in = -CUDART_INF, cX[3] = {0, 0, 0};
     double t_end = 0.0;
     int cb[3] = {0, 0, 0}, cbid = -1;
     double cTb[3] = {0, 0, 0};
@@ -384,18 +387,22 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                           : CUDART_INF;
     };
     auto enter_brick = [&](unsigned advanced, double tn) {
+        double m = -CUDART_INF;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             if (cs[a] == 0) continue;
             if (advanced & (1u << a)) {
                 const int cn = cs[a] > 0 ? cb[a] * 8 : cb[a] * 8 + 7;
                 cc[a] = cn;
-                cE[a] = tn;
+                m = fmax(m, tn);
                 cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a]);
             } else {
-                sync_axis(og[a], dg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], cE[a], cX[a]);
+                double E;
+                sync_axis(og[a], dg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], E, cX[a]);
+                m = fmax(m, E);
             }
         }
+        t_in = m;
     };
     auto walk_step = [&]() {
         if (cbid < 0) {  // empty brick: one brick step
@@ -418,8 +425,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             return;
         }
         ARTEMIS_STAT(1);
-        const double t0 = fmax(p.t_min, fmax(cE[0], fmax(cE[1], cE[2])));
-        const double t1 = fmin(p.t_max, fmin(cX[0], fmin(cX[1], cX[2])));
+        // next cell: every axis whose exit crossing is the minimum steps
+        const double tn = fmin(cX[0], fmin(cX[1], cX[2]));
+        const double t0 = fmax(p.t_min, t_in);
+        const double t1 = fmin(p.t_max, tn);
         const uint32_t m = spread3_small(cc[0] & 7) | (spread3_small(cc[1] & 7) << 1) |
                            (spread3_small(cc[2] & 7) << 2);
         const BrickRec &R = p.bm.recs[cbid];
@@ -429,12 +438,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                                   (uint32_t)__popc(word & ((1u << (m & 31u)) - 1u));
             enqueue_hit(leaf, t0, t1);
         }
-        // next cell: every axis whose exit crossing is the minimum steps
-        const double tn = fmin(cX[0], fmin(cX[1], cX[2]));
         if (!(tn < p.t_max) || !(tn < t_end)) {
             walking = false;
             return;
         }
+        t_in = tn;
         unsigned pend = (cX[0] == tn ? 1u : 0u) | (cX[1] == tn ? 2u : 0u) | (cX[2] == tn ? 4u : 0u);
         bool new_brick = false;
         while (pend) {
@@ -450,7 +458,6 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             for (int a = 0; a < 3; ++a)
                 if (a == k) {
                     cc[a] = ck;
-                    cE[a] = tn;
                     cX[a] = xn;
                     if (bchg) {  // the cell exit just crossed was this brick's exit plane
                         cb[a] = ck >> 3;
@@ -608,16 +615,18 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 }
             }
             t_end = t1;
+            t_in = -CUDART_INF;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (dg[a] == 0.0) {
                     cs[a] = 0;
                     cc[a] = (int)floor(og[a]);
-                    cE[a] = -CUDART_INF;
                     cX[a] = CUDART_INF;
                 } else {
                     cs[a] = dg[a] > 0.0 ? 1 : -1;
-                    sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], cE[a], cX[a]);
+                    double E;
+                    sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], E, cX[a]);
+                    t_in = fmax(t_in, E);
                 }
                 cb[a] = cc[a] >> 3;
             }
