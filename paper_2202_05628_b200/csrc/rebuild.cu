@@ -163,10 +163,18 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     const int64_t per = (n + 1023) / 1024;
     const int64_t lo = t * per, hi = min(n, lo + per);
     uint32_t xa = 0, xb = 0;
-#pragma unroll 8
-    for (int64_t i = lo; i < hi; ++i) {  // unrolled: the loads of a batch overlap
-        xa += a[i];
-        xb += b[i];
+    for (int64_t base = lo; base < hi; base += 8) {  // batches of 8 independent loads
+        uint32_t ta[8], tb[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            ta[k] = base + k < hi ? a[base + k] : 0u;
+            tb[k] = base + k < hi ? b[base + k] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            xa += ta[k];
+            xb += tb[k];
+        }
     }
     uint32_t ia = xa, ib = xb;
 #pragma unroll
@@ -200,13 +208,22 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     __syncthreads();
     uint32_t ea = (wid ? sa[wid - 1] : 0u) + ia - xa;
     uint32_t eb = (wid ? sb[wid - 1] : 0u) + ib - xb;
-#pragma unroll 8
-    for (int64_t i = lo; i < hi; ++i) {
-        const uint32_t va = a[i], vb = b[i];
-        a[i] = ea;
-        b[i] = eb;
-        ea += va;
-        eb += vb;
+    for (int64_t base = lo; base < hi; base += 8) {
+        uint32_t ta[8], tb[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            ta[k] = base + k < hi ? a[base + k] : 0u;
+            tb[k] = base + k < hi ? b[base + k] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (base + k < hi) {
+                a[base + k] = ea;
+                b[base + k] = eb;
+            }
+            ea += ta[k];
+            eb += tb[k];
+        }
     }
     if (t == 1023) {
         *total_a = (int32_t)ea;

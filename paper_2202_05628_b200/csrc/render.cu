@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         rf.exact_only = false;
         rf.cmax = 0.0f;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
+        for (int a = 0; a < 3 && !kDDA; ++a) {  // the fp32 box filter of the tree DFS
             if (dg[a] == 0.0) {
                 rf.exact_only = true;
                 rf.inv[a] = rf.o_inv[a] = 0.0f;
@@ -691,8 +691,12 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             double so[3], sd[3], sw[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                so[a] = __shfl_sync(0xffffffffu, og[a], src);
-                sd[a] = __shfl_sync(0xffffffffu, dg[a], src);
+                if constexpr (!kDDA) {  // the cell walk already holds the exact interval
+                    so[a] = __shfl_sync(0xffffffffu, og[a], src);
+                    sd[a] = __shfl_sync(0xffffffffu, dg[a], src);
+                } else {
+                    so[a] = sd[a] = 0.0;
+                }
                 if (kMode != kCount) sw[a] = s_dw[3 * (wbase + src) + a];
             }
             if (has && kMode != kCount) {
