@@ -116,6 +116,54 @@ __device__ __forceinline__ float4 ld_row(const float4 *p, uint64_t pol) {
 #endif
 }
 
+// Conservative fp32 cull of a camera ray against the leaf-cell AABB grown by
+// one cell on every side. fp32 rounding moves the ray by far less than a
+// cell over the grid (|error| <~ 1e-6 x (|o| + |d t|) cells), so "misses the
+// grown box in fp32" implies "misses the box exactly": such a pixel has no
+// hit (alpha 0, depth +inf, F 0) and the exact fp64 ray is never built. A
+// nearly axis-parallel fp32 direction is not culled (left to the exact path).
+__device__ __forceinline__ bool ray_misses_aabb(const artemis_camera &c, int u, int v,
+                                                const int32_t *aabb) {
+    const float c0 = ((float)u + 0.5f - (float)c.cx) / (float)c.fx;
+    const float c1 = ((float)v + 0.5f - (float)c.cy) / (float)c.fy;
+    float t0 = 0.0f, t1 = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float d = ((float)c.R[3 * a] * c0 + (float)c.R[3 * a + 1] * c1 + (float)c.R[3 * a + 2]) /
+                        (float)c.cell[a];
+        const float o = (float)((c.origin[a] - c.lo[a]) / c.cell[a]);
+        const float lo = (float)(__ldg(aabb + a) - 1), hi = (float)(__ldg(aabb + 3 + a) + 1);
+        if (fabsf(d) < 1e-4f) return false;  // nearly parallel: exact path decides
+        float ta = (lo - o) / d, tb = (hi - o) / d;
+        if (ta > tb) {
+            const float s = ta;
+            ta = tb;
+            tb = s;
+        }
+        t0 = fmaxf(t0, ta);
+        t1 = fminf(t1, tb);
+    }
+    return t0 > t1;
+}
+
+// A camera pixel without hits: alpha 0 and depth +inf (F stays cleared).
+__device__ __forceinline__ void write_empty_pixel(const RenderArgs &p, int64_t ray, int rv) {
+    if (p.n_views > 1) {
+        if (p.A64) {
+            static_cast<double *>(p.Av[rv])[ray] = 0.0;
+            static_cast<double *>(p.Dv[rv])[ray] = CUDART_INF;
+        } else {
+            static_cast<float *>(p.Av[rv])[ray] = 0.0f;
+            static_cast<float *>(p.Dv[rv])[ray] = CUDART_INF_F;
+        }
+        return;
+    }
+    if (p.A64) p.A64[ray] = 0.0;
+    if (p.A32) p.A32[ray] = 0.0f;
+    if (p.D64) p.D64[ray] = CUDART_INF;
+    if (p.D32) p.D32[ray] = CUDART_INF_F;
+}
+
 // Ray/box overlap of the child box packed in (w0, w1, w2) within
 // [t_min, t_max]; exact port of the slab test (_core.pyx:252-285).
 __device__ __forceinline__ bool clip_exact(uint32_t w0, uint32_t w1, uint32_t w2,
@@ -542,6 +590,15 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             if (py < cam.height && px < cam.width) {
                 ARTEMIS_DCHECK(tile >= 0 && tile < n_tiles);
                 ray = (int64_t)py * cam.width + px;
+                if constexpr (kDDA && kMode == kRender) {
+                    if (ray_misses_aabb(cam, px, py, p.bm.aabb)) {
+                        // no leaf can be hit: the pixel's result is F = 0 (cleared),
+                        // alpha = 0, depth = +inf, written now; the lane stays free
+                        write_empty_pixel(p, ray, rv);
+                        ray = -1;
+                        return;
+                    }
+                }
                 camera_ray(cam, px, py, og, dg, dw);
             }
         } else {
