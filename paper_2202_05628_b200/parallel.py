@@ -198,4 +198,13 @@ class PeerAssembly:
         return (self.F, self.A, self.D) if self.rank == self.dst else None
 
     def close(self):
+        """Detach the pipeline from the peer maps. Every rank drops its IPC
+        mapping before the root may free the maps (barrier), so no process
+        tears down memory another one still maps."""
         self.fp.set_output_peer(None)
+        self.fp.stream.synchronize()
+        if self.rank != self.dst:
+            self.F = self.A = self.D = None
+            torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()

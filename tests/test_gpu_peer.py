@@ -52,8 +52,11 @@ def _worker(rank, world, port, out_path, maps64):
         ref.close()
         open(out_path, "w").write("ok")
     dist.barrier()
-    asm.close()
+    asm.close()  # mappings released on every rank before the root's maps go
     fp.close()
+    del asm
+    torch.cuda.synchronize()
+    dist.barrier()
     dist.destroy_process_group()
 
 
