@@ -77,6 +77,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_STREAM_OUT
 #define ARTEMIS_STREAM_OUT 0  // 1: output maps stored evict-first (st.global.cs)
 #endif
+#ifndef ARTEMIS_CULL
+#define ARTEMIS_CULL 0  // 1: fp32 AABB cull of camera rays (measured slower: DESIGN.md)
+#endif
 #ifndef ARTEMIS_FLAT_SHADE
 #define ARTEMIS_FLAT_SHADE 0  // 1: shade a flat member list per level (see phase C)
 #endif
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             if (py < cam.height && px < cam.width) {
                 ARTEMIS_DCHECK(tile >= 0 && tile < n_tiles);
                 ray = (int64_t)py * cam.width + px;
-                if constexpr (kDDA && kMode == kRender) {
+                if constexpr (kDDA && kMode == kRender && ARTEMIS_CULL) {
                     if (ray_misses_aabb(cam, px, py, p.bm.aabb)) {
                         // no leaf can be hit: the pixel's result is F = 0 (cleared),
                         // alpha = 0, depth = +inf, written now; the lane stays free

@@ -10,6 +10,7 @@ VARIANTS = {
     "checks": ("ARTEMIS_DEBUG_CHECKS=1",),
     "sout": ("ARTEMIS_STREAM_OUT=1",),
     "flat": ("ARTEMIS_FLAT_SHADE=1",),
+    "nocull": ("ARTEMIS_CULL=0",),
     "flat_nopf": ("ARTEMIS_FLAT_SHADE=1", "ARTEMIS_ROW_PREFETCH=0"),
     "rhint": ("ARTEMIS_ROW_HINT=1",),
     "sout_rhint": ("ARTEMIS_STREAM_OUT=1", "ARTEMIS_ROW_HINT=1"),
