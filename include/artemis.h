@@ -521,6 +521,14 @@ int artemis_host_checksum(const void *data /* host */, size_t bytes, int threads
  * race/determinism tests vary it to change the ray-to-warp schedule. */
 int artemis_debug_set_render_blocks(int max_blocks);
 
+/* artemis_host_widen_f32 (host, synchronous): dst[r][c] = (double)src[r][c]
+ * for a rows x cols block (row pitches in elements) on up to `threads` host
+ * threads -- the fp32 -> fp64 step of the per-frame API's FrameBuffers
+ * (the reference's features are float64, render.py:359-363). */
+int artemis_host_widen_f32(const float *src /* host */, int64_t rows, int64_t cols,
+                           int64_t src_pitch, double *dst /* host */, int64_t dst_pitch,
+                           int threads);
+
 /* Synchronous device -> host copy (parity helpers). */
 int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);
 

@@ -545,7 +545,7 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
         f->n_words = (bricks + 31) / 32;
         rc = rc ? rc : dev_alloc(&f->bmask, (size_t)f->n_words * 32 * 16 * 4);
         rc = rc ? rc : dev_alloc(&f->bocc, (size_t)f->n_words * 4);
-        rc = rc ? rc : dev_alloc(&f->wtmp, (size_t)f->n_words * (8 + 32 * 4));
+        rc = rc ? rc : dev_alloc(&f->wtmp, (size_t)f->n_words * (8 + 32 * 4 + 8));
         rc = rc ? rc : dev_alloc(&f->wkey, (size_t)n * 8);
         if (!rc && (cudaMemset(f->bmask, 0, (size_t)f->n_words * 32 * 16 * 4) != cudaSuccess ||
                     cudaMemset(f->bocc, 0, (size_t)f->n_words * 4) != cudaSuccess))

@@ -100,3 +100,37 @@ extern "C" int artemis_host_checksum(const void *data, size_t bytes, int threads
     out[1] = avalanche(h1 ^ h0);
     return ARTEMIS_OK;
 }
+
+// fp32 -> fp64 widening of a row-strided block on several host threads (the
+// reference returns FrameBuffers.features as float64, render.py:359-363):
+// rows x cols floats at src (row pitch src_pitch floats) into dst (row pitch
+// dst_pitch doubles). Exact (every float is a double).
+extern "C" int artemis_host_widen_f32(const float *src, int64_t rows, int64_t cols,
+                                      int64_t src_pitch, double *dst, int64_t dst_pitch,
+                                      int threads) {
+    if (rows < 0 || cols < 0 || (rows && cols && (!src || !dst))) return ARTEMIS_ERR_ARG;
+    if (!rows || !cols) return ARTEMIS_OK;
+    auto work = [&](int64_t r0, int64_t r1) {
+        for (int64_t r = r0; r < r1; ++r) {
+            const float *s = src + r * src_pitch;
+            double *d = dst + r * dst_pitch;
+            for (int64_t c = 0; c < cols; ++c) d[c] = (double)s[c];
+        }
+    };
+    const int64_t total = rows * cols;
+    int64_t nt = std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : 1,
+                                                        total / (1 << 18)));
+    nt = std::min<int64_t>(nt, rows);
+    if (nt <= 1) {
+        work(0, rows);
+        return ARTEMIS_OK;
+    }
+    std::vector<std::thread> pool;
+    const int64_t per = (rows + nt - 1) / nt;
+    for (int64_t t = 0; t < nt; ++t) {
+        const int64_t r0 = t * per, r1 = std::min(rows, r0 + per);
+        if (r0 < r1) pool.emplace_back(work, r0, r1);
+    }
+    for (auto &th : pool) th.join();
+    return ARTEMIS_OK;
+}

@@ -95,7 +95,8 @@ __device__ __forceinline__ void word_aabb(uint32_t m, int q, int bx, int by, int
 __global__ void count_kernel(const uint32_t *__restrict__ bocc,
                              const uint32_t *__restrict__ bmask, int64_t n_words,
                              uint32_t *__restrict__ n_bricks, uint32_t *__restrict__ n_cells,
-                             uint32_t *__restrict__ bpre, int32_t *aabb) {
+                             uint32_t *__restrict__ bpre, uint32_t *__restrict__ blk_bricks,
+                             uint32_t *__restrict__ blk_cells, int32_t *aabb) {
     __shared__ int red[6][kCountThreads / 32];
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -123,12 +124,34 @@ __global__ void count_kernel(const uint32_t *__restrict__ bocc,
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
+    // block-level exclusive offsets of the block's words (8 words per block);
+    // the block totals are scanned across blocks by scan2_kernel
+    __shared__ uint32_t s_nb[kCountThreads / 32], s_nc[kCountThreads / 32];
+    if (lane == 31) {
+        s_nb[wid] = __popc(occ);
+        s_nc[wid] = incl;
+    }
+    __syncthreads();
     if (w < n_words) {
         bpre[32 * w + lane] = incl - c;
-        if (lane == 31) {
-            n_bricks[w] = __popc(occ);
-            n_cells[w] = incl;
+        if (lane == 0) {
+            uint32_t ob = 0, oc = 0;
+            for (int v = 0; v < wid; ++v) {
+                ob += s_nb[v];
+                oc += s_nc[v];
+            }
+            n_bricks[w] = ob;  // exclusive within the block
+            n_cells[w] = oc;
         }
+    }
+    if (threadIdx.x == 0) {
+        uint32_t tb = 0, tc = 0;
+        for (int v = 0; v < kCountThreads / 32; ++v) {
+            tb += s_nb[v];
+            tc += s_nc[v];
+        }
+        blk_bricks[blockIdx.x] = tb;
+        blk_cells[blockIdx.x] = tc;
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -238,6 +261,8 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
 __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restrict__ bmask,
                             int64_t n_bricks_dense, const uint32_t *__restrict__ rec_base,
                             const uint32_t *__restrict__ cell_base,
+                            const uint32_t *__restrict__ blk_bricks,
+                            const uint32_t *__restrict__ blk_cells,
                             const uint32_t *__restrict__ bpre, BrickRec *__restrict__ recs,
                             int32_t *__restrict__ table, int dx, int dy,
                             unsigned long long *__restrict__ wkey,
@@ -249,8 +274,9 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
     const int j = (int)(b & 31);
     const uint32_t occ = bocc[w];
     if (!((occ >> j) & 1u)) return;  // warp-uniform
-    const uint32_t rec = rec_base[w] + __popc(occ & ((1u << j) - 1u));
-    const uint32_t first = cell_base[w] + bpre[b];
+    const int64_t blk = w / (kCountThreads / 32);
+    const uint32_t rec = blk_bricks[blk] + rec_base[w] + __popc(occ & ((1u << j) - 1u));
+    const uint32_t first = blk_cells[blk] + cell_base[w] + bpre[b];
     uint32_t *mk = bmask + b * 16;
     BrickRec &R = recs[rec];
     const uint32_t m = lane < 16 ? mk[lane] : 0u;
@@ -335,11 +361,12 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
     ARTEMIS_TRY(cudaMemsetAsync(aabb + 3, 0x80, 3 * sizeof(int32_t), st));
     const int wb = (int)ceil_div<int64_t>(n_words * 32, kCountThreads);
     uint32_t *bpre = wtmp + 2 * n_words;  // per dense brick: cells before it in its word
-    count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bpre, aabb);
-    scan2_kernel<<<1, 1024, 0, st>>>(nc, nb, n_words, n_recs, n_live);
+    uint32_t *bb = bpre + 32 * n_words, *bc = bb + wb;  // per count block: bricks, cells
+    count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bpre, bb, bc, aabb);
+    scan2_kernel<<<1, 1024, 0, st>>>(bc, bb, wb, n_recs, n_live);
     const int64_t n_bricks = n_words * 32;
     emit_kernel<<<(int)ceil_div<int64_t>(n_bricks * 32, kCountThreads), kCountThreads, 0, st>>>(
-        bocc, bmask, n_bricks, nb, nc, bpre, recs, table, dims[0], dims[1], wkey, winners);
+        bocc, bmask, n_bricks, nb, nc, bb, bc, bpre, recs, table, dims[0], dims[1], wkey, winners);
     const int vb = (int)ceil_div<int64_t>(std::max<int64_t>(n, n_words), kCountThreads);
     slot_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
                                               dims[1], live_codes, wkey, bocc, n_words);

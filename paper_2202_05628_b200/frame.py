@@ -164,6 +164,51 @@ class FramePipeline:
             cur.wait_stream(self.stream)  # consumers on the caller's stream see the frame
         return F, A, D
 
+    def host_frame64(self, F, A, D, width: int, height: int):
+        """A maps64 frame on this pipeline's stream -> freshly allocated host
+        arrays in the reference's FrameBuffers layout (render.py:359-363):
+        features float64 (h, w, C), alpha and depth float64 (h, w). Only the
+        covered pixels' bounding box of F crosses PCIe (pinned staging) and is
+        widened to float64 natively on several host threads; the rest of the
+        features array is zero (np.zeros pages, untouched)."""
+        L = _lib.lib()
+        C_ = self.channels
+        n = width * height
+        key = ("api64", width, height)
+        if not hasattr(self, "_api_bufs"):
+            self._api_bufs = {}
+        if key not in self._api_bufs:
+            with torch.cuda.stream(self.stream):
+                dbox = torch.empty(4, dtype=torch.int32, device="cuda")
+            self._api_bufs[key] = dict(
+                dbox=dbox, box=torch.empty(4, dtype=torch.int32, pin_memory=True),
+                F=torch.empty(n * C_, dtype=torch.float32, pin_memory=True),
+                A=torch.empty(n, dtype=torch.float64, pin_memory=True),
+                D=torch.empty(n, dtype=torch.float64, pin_memory=True))
+        b = self._api_bufs[key]
+        st = self.stream.cuda_stream or None
+        check(L.artemis_frame_bbox(ptr(A), ptr(D), 1, width, height, ptr(b["dbox"]), st),
+              "frame_bbox")
+        with torch.cuda.stream(self.stream):
+            b["box"].copy_(b["dbox"], non_blocking=True)
+            b["A"].copy_(A.reshape(-1), non_blocking=True)
+            b["D"].copy_(D.reshape(-1), non_blocking=True)
+        self.stream.synchronize()
+        x0, y0, x1, y1 = (int(v) for v in b["box"])
+        features = np.zeros((height, width, C_), dtype=np.float64)
+        if x1 >= 0:
+            rows, cols = y1 - y0 + 1, (x1 - x0 + 1) * C_
+            check(L.artemis_copy_rect_d2h(b["F"].data_ptr(), ptr(F), width * C_ * 4, x0 * C_ * 4,
+                                          cols * 4, y0, rows, st), "copy_rect")
+            self.stream.synchronize()
+            off = (y0 * width + x0) * C_
+            check(L.artemis_host_widen_f32(b["F"].data_ptr() + 4 * off, rows, cols, width * C_,
+                                           features.ctypes.data + 8 * off, width * C_,
+                                           max(1, min(16, os.cpu_count() or 1))), "widen")
+        alpha = b["A"].numpy().reshape(height, width).copy()
+        depth = b["D"].numpy().reshape(height, width).copy()
+        return features, alpha, depth
+
     def view_outputs(self, width: int, height: int, n: int, maps64: bool = False):
         """Persistent per-view device outputs for run_views."""
         key = ("views", width, height, n, bool(maps64))

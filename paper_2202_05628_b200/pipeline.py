@@ -429,10 +429,8 @@ def _frame_device(asset, pose, camera, opts, timed: bool):
         warp = warp_voxels(asset.voxels, asset.weights, asset.skeleton, pose)
         raise EmptyWarpError(warp.dropped)
     t1 = time.perf_counter()
-    h, w = cam.height, cam.width
-    frame = T.make("FrameBuffers",
-                   features=download(F).astype(np.float64).reshape(h, w, fp.channels),
-                   alpha=download(A).reshape(h, w), depth=download(D).reshape(h, w))
+    features, alpha, depth = fp.host_frame64(F, A, D, cam.width, cam.height)
+    frame = T.make("FrameBuffers", features=features, alpha=alpha, depth=depth)
     times = None
     if timed:
         host = time.perf_counter() - t1

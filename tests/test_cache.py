@@ -73,3 +73,19 @@ def test_content_key_and_policy(lib):
         K.set_cache_policy("content")
     with pytest.raises(ValueError):
         K.set_cache_policy("sampled")
+
+
+def test_host_widen_rect(lib):
+    """artemis_host_widen_f32: exact fp32 -> fp64 of a row-strided block
+    (the per-frame API's FrameBuffers.features readout)."""
+    rng = np.random.default_rng(2)
+    src = rng.normal(size=(300, 700)).astype(np.float32)
+    dst = np.zeros((300, 900), dtype=np.float64)
+    r0, c0, rows, cols = 17, 40, 250, 600
+    off_s = r0 * 700 + c0
+    off_d = r0 * 900 + c0 + 100
+    assert lib.artemis_host_widen_f32(src.ctypes.data + 4 * off_s, rows, cols, 700,
+                                      dst.ctypes.data + 8 * off_d, 900, 8) == 0
+    want = np.zeros_like(dst)
+    want[r0:r0 + rows, c0 + 100:c0 + 100 + cols] = src[r0:r0 + rows, c0:c0 + cols]
+    assert np.array_equal(dst, want)
