@@ -254,12 +254,12 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     }
 }
 
-// one warp per brick (most exit at once: unoccupied): an occupied brick's
-// record (mask, per-word prefix, first leaf), its table entry and its live
-// slots (initialised for slot/winner, coalesced); clears its dense mask for
-// the next frame
+// one warp per bitmap word; its occupied bricks one after another (warp-
+// uniform loop): lanes 0..15 write the brick record's mask words and per-word
+// prefix (and clear the dense mask for the next frame), lane 0 the first leaf
+// and the table entry, all lanes initialise the brick's live slots (coalesced)
 __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restrict__ bmask,
-                            int64_t n_bricks_dense, const uint32_t *__restrict__ rec_base,
+                            int64_t n_words, const uint32_t *__restrict__ rec_base,
                             const uint32_t *__restrict__ cell_base,
                             const uint32_t *__restrict__ blk_bricks,
                             const uint32_t *__restrict__ blk_cells,
@@ -267,40 +267,47 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
                             int32_t *__restrict__ table, int dx, int dy,
                             unsigned long long *__restrict__ wkey,
                             uint32_t *__restrict__ widx) {
-    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (b >= n_bricks_dense) return;
-    const int64_t w = b >> 5;
-    const int j = (int)(b & 31);
+    if (w >= n_words) return;
     const uint32_t occ = bocc[w];
-    if (!((occ >> j) & 1u)) return;  // warp-uniform
+    if (!occ) return;  // warp-uniform
     const int64_t blk = w / (kCountThreads / 32);
-    const uint32_t rec = blk_bricks[blk] + rec_base[w] + __popc(occ & ((1u << j) - 1u));
-    const uint32_t first = blk_cells[blk] + cell_base[w] + bpre[b];
-    uint32_t *mk = bmask + b * 16;
-    BrickRec &R = recs[rec];
-    const uint32_t m = lane < 16 ? mk[lane] : 0u;
-    uint32_t pre = __popc(m);  // inclusive scan of the word popcounts
+    const uint32_t rec0 = blk_bricks[blk] + rec_base[w];
+    const uint32_t cell0 = blk_cells[blk] + cell_base[w];
+    const uint32_t my_pre = bpre[32 * w + lane];  // lane j: cells before brick j in the word
+    uint32_t todo = occ;
+    while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const u64 b = (u64)(32 * w + j);
+        const uint32_t rec = rec0 + __popc(occ & ((1u << j) - 1u));
+        const uint32_t first = cell0 + __shfl_sync(0xffffffffu, my_pre, j);
+        uint32_t *mk = bmask + b * 16;
+        BrickRec &R = recs[rec];
+        const uint32_t m = lane < 16 ? mk[lane] : 0u;
+        uint32_t pre = __popc(m);  // inclusive scan of the word popcounts
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += y;
-    }
-    const uint32_t run = __shfl_sync(0xffffffffu, pre, 15);
-    if (lane < 16) {
-        R.mask[lane] = m;
-        R.prefix[lane] = (uint16_t)(pre - __popc(m));
-        mk[lane] = 0u;  // ready for the next frame
-    }
-    if (lane == 0) {
-        R.first = first;
-        const int bx = (int)compact_bits3((u64)b), by = (int)compact_bits3((u64)b >> 1),
-                  bz = (int)compact_bits3((u64)b >> 2);
-        table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
-    }
-    for (uint32_t k = lane; k < run; k += 32) {  // the brick's live slots
-        wkey[first + k] = 0ull;
-        widx[first + k] = 0xFFFFFFFFu;
+        for (int o = 1; o < 16; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const uint32_t run = __shfl_sync(0xffffffffu, pre, 15);
+        if (lane < 16) {
+            R.mask[lane] = m;
+            R.prefix[lane] = (uint16_t)(pre - __popc(m));
+            mk[lane] = 0u;  // ready for the next frame
+        }
+        if (lane == 0) {
+            R.first = first;
+            const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
+                      bz = (int)compact_bits3(b >> 2);
+            table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
+        }
+        for (uint32_t k = lane; k < run; k += 32) {  // the brick's live slots
+            wkey[first + k] = 0ull;
+            widx[first + k] = 0xFFFFFFFFu;
+        }
     }
 }
 
@@ -364,9 +371,8 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
     uint32_t *bb = bpre + 32 * n_words, *bc = bb + wb;  // per count block: bricks, cells
     count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bpre, bb, bc, aabb);
     scan2_kernel<<<1, 1024, 0, st>>>(bc, bb, wb, n_recs, n_live);
-    const int64_t n_bricks = n_words * 32;
-    emit_kernel<<<(int)ceil_div<int64_t>(n_bricks * 32, kCountThreads), kCountThreads, 0, st>>>(
-        bocc, bmask, n_bricks, nb, nc, bb, bc, bpre, recs, table, dims[0], dims[1], wkey, winners);
+    emit_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bb, bc, bpre, recs,
+                                              table, dims[0], dims[1], wkey, winners);
     const int vb = (int)ceil_div<int64_t>(std::max<int64_t>(n, n_words), kCountThreads);
     slot_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
                                               dims[1], live_codes, wkey, bocc, n_words);

@@ -11,6 +11,9 @@ VARIANTS = {
     "sout": ("ARTEMIS_STREAM_OUT=1",),
     "flat": ("ARTEMIS_FLAT_SHADE=1",),
     "nocull": ("ARTEMIS_CULL=0",),
+    "q4b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48", "ARTEMIS_MIN_BLOCKS=5"),
+    "q4t40b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=40", "ARTEMIS_MIN_BLOCKS=5"),
+    "q4t56b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=56", "ARTEMIS_MIN_BLOCKS=5"),
     "flat_nopf": ("ARTEMIS_FLAT_SHADE=1", "ARTEMIS_ROW_PREFETCH=0"),
     "rhint": ("ARTEMIS_ROW_HINT=1",),
     "sout_rhint": ("ARTEMIS_STREAM_OUT=1", "ARTEMIS_ROW_HINT=1"),

@@ -45,6 +45,7 @@ for k in last:
     t = k["gpu__time_duration.sum"]
     dram = k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0)
     gbs = dram / t / 1e9 if t else 0.0
-    print(f"{k['name'][5:49]:<44} {t * 1e6:8.1f} {100 * t / tot:5.1f}% {gbs:9.0f} "
+    name = k["name"][5:] if k["name"].startswith("void ") else k["name"]
+    print(f"{name[:44]:<44} {t * 1e6:8.1f} {100 * t / tot:5.1f}% {gbs:9.0f} "
           f"{100 * gbs / peak:7.1f}% {k.get('lts__t_sector_hit_rate.pct', 0):6.1f}% "
           f"{dram / 1e6:8.1f} {k.get('lts__t_bytes.sum', 0) / 1e6:8.1f}")
