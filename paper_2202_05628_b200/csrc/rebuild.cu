@@ -254,61 +254,75 @@ __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, i
     }
 }
 
-// one warp per bitmap word; its occupied bricks one after another (warp-
-// uniform loop): lanes 0..15 write the brick record's mask words and per-word
-// prefix (and clear the dense mask for the next frame), lane 0 the first leaf
-// and the table entry, all lanes initialise the brick's live slots (coalesced)
+// one warp per bitmap word, one lane per brick (all bricks of the word in
+// parallel): an occupied brick's record (mask, per-word prefix, first leaf),
+// its table entry, and its dense mask cleared for the next frame. The live
+// slots' winner keys need no initialisation here: finish_kernel resets the
+// ones a frame used after the tree is built (they start zeroed at creation).
 __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restrict__ bmask,
                             int64_t n_words, const uint32_t *__restrict__ rec_base,
                             const uint32_t *__restrict__ cell_base,
                             const uint32_t *__restrict__ blk_bricks,
                             const uint32_t *__restrict__ blk_cells,
                             const uint32_t *__restrict__ bpre, BrickRec *__restrict__ recs,
-                            int32_t *__restrict__ table, int dx, int dy,
-                            unsigned long long *__restrict__ wkey,
-                            uint32_t *__restrict__ widx) {
+                            int32_t *__restrict__ table, int dx, int dy) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= n_words) return;
     const uint32_t occ = bocc[w];
-    if (!occ) return;  // warp-uniform
+    if (!((occ >> lane) & 1u)) return;
     const int64_t blk = w / (kCountThreads / 32);
-    const uint32_t rec0 = blk_bricks[blk] + rec_base[w];
-    const uint32_t cell0 = blk_cells[blk] + cell_base[w];
-    const uint32_t my_pre = bpre[32 * w + lane];  // lane j: cells before brick j in the word
-    uint32_t todo = occ;
-    while (todo) {
-        const int j = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const u64 b = (u64)(32 * w + j);
-        const uint32_t rec = rec0 + __popc(occ & ((1u << j) - 1u));
-        const uint32_t first = cell0 + __shfl_sync(0xffffffffu, my_pre, j);
-        uint32_t *mk = bmask + b * 16;
-        BrickRec &R = recs[rec];
-        const uint32_t m = lane < 16 ? mk[lane] : 0u;
-        uint32_t pre = __popc(m);  // inclusive scan of the word popcounts
+    const uint32_t rec = blk_bricks[blk] + rec_base[w] + __popc(occ & ((1u << lane) - 1u));
+    const u64 b = (u64)(32 * w + lane);
+    uint4 *mk = reinterpret_cast<uint4 *>(bmask + b * 16);
+    BrickRec &R = recs[rec];
+    uint4 *rm = reinterpret_cast<uint4 *>(R.mask);
+    uint32_t pf[16];
+    uint32_t run = 0;
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
-            if (lane >= o) pre += y;
-        }
-        const uint32_t run = __shfl_sync(0xffffffffu, pre, 15);
-        if (lane < 16) {
-            R.mask[lane] = m;
-            R.prefix[lane] = (uint16_t)(pre - __popc(m));
-            mk[lane] = 0u;  // ready for the next frame
-        }
-        if (lane == 0) {
-            R.first = first;
-            const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
-                      bz = (int)compact_bits3(b >> 2);
-            table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
-        }
-        for (uint32_t k = lane; k < run; k += 32) {  // the brick's live slots
-            wkey[first + k] = 0ull;
-            widx[first + k] = 0xFFFFFFFFu;
-        }
+    for (int q4 = 0; q4 < 4; ++q4) {
+        const uint4 v = mk[q4];
+        rm[q4] = v;
+        mk[q4] = make_uint4(0u, 0u, 0u, 0u);  // ready for the next frame
+        pf[4 * q4] = run;
+        run += __popc(v.x);
+        pf[4 * q4 + 1] = run;
+        run += __popc(v.y);
+        pf[4 * q4 + 2] = run;
+        run += __popc(v.z);
+        pf[4 * q4 + 3] = run;
+        run += __popc(v.w);
     }
+    uint4 *rp = reinterpret_cast<uint4 *>(R.prefix);
+    rp[0] = make_uint4(pf[0] | (pf[1] << 16), pf[2] | (pf[3] << 16), pf[4] | (pf[5] << 16),
+                       pf[6] | (pf[7] << 16));
+    rp[1] = make_uint4(pf[8] | (pf[9] << 16), pf[10] | (pf[11] << 16), pf[12] | (pf[13] << 16),
+                       pf[14] | (pf[15] << 16));
+    R.first = blk_cells[blk] + cell_base[w] + bpre[b];
+    const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
+              bz = (int)compact_bits3(b >> 2);
+    table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
+}
+
+// after the Karras build consumed them: the winners out of the atomicMin
+// scratch into the frame's winner array, and the scratch slots the frame
+// used reset for the next frame
+__global__ void finish_kernel(const int32_t *__restrict__ n_live, uint32_t *__restrict__ widx,
+                              unsigned long long *__restrict__ wkey,
+                              uint32_t *__restrict__ winners) {
+    const int64_t n = *n_live;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        winners[i] = widx[i];
+        widx[i] = 0xFFFFFFFFu;
+        wkey[i] = 0ull;
+    }
+}
+
+int counting_finish(const int32_t *n_live, uint32_t *widx, unsigned long long *wkey,
+                    uint32_t *winners, cudaStream_t st) {
+    finish_kernel<<<num_sms() * 4, 256, 0, st>>>(n_live, widx, wkey, winners);
+    return ARTEMIS_LAUNCHED();
 }
 
 // live-cell rank of an in-bounds voxel's key (from its brick record)
@@ -372,7 +386,7 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
     count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bpre, bb, bc, aabb);
     scan2_kernel<<<1, 1024, 0, st>>>(bc, bb, wb, n_recs, n_live);
     emit_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bb, bc, bpre, recs,
-                                              table, dims[0], dims[1], wkey, winners);
+                                              table, dims[0], dims[1]);
     const int vb = (int)ceil_div<int64_t>(std::max<int64_t>(n, n_words), kCountThreads);
     slot_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
                                               dims[1], live_codes, wkey, bocc, n_words);
