@@ -59,43 +59,58 @@ __device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick 
     } while (0)
 #endif
 
-__device__ __forceinline__ double crossing(int k, double o, double d) {
+#ifndef ARTEMIS_RCP_CROSSING
+#define ARTEMIS_RCP_CROSSING 0
+#endif
+// r = __drcp_rn(d), the correctly rounded reciprocal of the divisor (per ray,
+// per axis). With ARTEMIS_RCP_CROSSING the quotient is q = RN(n r) corrected
+// once with the exact residual n - q d (one FMA): RN(q + (n - q d) r) is
+// RN(n / d) for a correctly rounded r (Markstein's theorem), i.e. exactly
+// __ddiv_rn's result, in three dependent fp64 ops.
+__device__ __forceinline__ double crossing(int k, double o, double d, double r) {
     ARTEMIS_STAT(0);
+#if ARTEMIS_RCP_CROSSING
+    const double n = __dadd_rn((double)k, -o);
+    const double q = __dmul_rn(n, r);
+    return __fma_rn(__fma_rn(-q, d, n), r, q);
+#else
+    (void)r;
     return __ddiv_rn(__dadd_rn((double)k, -o), d);
+#endif
 }
 
 // Slab of one axis that contains distance t (entry <= t < exit), searched
 // from an estimate inside [cmin, cmax]; returns its exact entry/exit.
-__device__ __forceinline__ void sync_axis(double o, double d, double t, int cmin, int cmax,
-                                          int &c, double &E, double &X) {
+__device__ __forceinline__ void sync_axis(double o, double d, double r, double t, int cmin,
+                                          int cmax, int &c, double &E, double &X) {
     ARTEMIS_STAT(3);
     const double est = floor(o + t * d);
     c = est < (double)cmin ? cmin : est > (double)cmax ? cmax : (int)est;
     if (d > 0.0) {  // slab c = [cross(c), cross(c+1))
-        double lo = crossing(c, o, d);
+        double lo = crossing(c, o, d, r);
         while (c > cmin && lo > t) {
             --c;
-            lo = crossing(c, o, d);
+            lo = crossing(c, o, d, r);
         }
-        double hi = crossing(c + 1, o, d);
+        double hi = crossing(c + 1, o, d, r);
         while (c < cmax && hi <= t) {
             ++c;
             lo = hi;
-            hi = crossing(c + 1, o, d);
+            hi = crossing(c + 1, o, d, r);
         }
         E = lo;
         X = hi;
     } else {  // slab c = [cross(c+1), cross(c))
-        double en = crossing(c + 1, o, d);
+        double en = crossing(c + 1, o, d, r);
         while (c < cmax && en > t) {
             ++c;
-            en = crossing(c + 1, o, d);
+            en = crossing(c + 1, o, d, r);
         }
-        double ex = crossing(c, o, d);
+        double ex = crossing(c, o, d, r);
         while (c > cmin && ex <= t) {
             --c;
             en = ex;
-            ex = crossing(c, o, d);
+            ex = crossing(c, o, d, r);
         }
         E = en;
         X = ex;

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     int64_t ray = -1;
     bool walking = false;  // DFS not exhausted
     double og[3], dg[3];
+    double rg[3] = {0.0, 0.0, 0.0};  // correctly rounded 1/dg (ARTEMIS_RCP_CROSSING)
     RayF rf;
     // exact cell walk state (kDDA): current cell, step signs, exact entry /
     // exit crossing per axis, the leaf AABB exit, the cached brick
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // while inside an occupied brick. Empty bricks cost one crossing each;
     // entering an occupied brick re-derives the other axes' cells there.
     auto brick_exit = [&](int a) {  // exact crossing of the current brick's exit plane on axis a
-        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a])
+        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a], rg[a])
                           : CUDART_INF;
     };
     auto enter_brick = [&](unsigned advanced, double tn) {
@@ -446,10 +447,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const int cn = cs[a] > 0 ? cb[a] * 8 : cb[a] * 8 + 7;
                 cc[a] = cn;
                 m = fmax(m, tn);
-                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a]);
+                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a], rg[a]);
             } else {
                 double E;
-                sync_axis(og[a], dg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], E, cX[a]);
+                sync_axis(og[a], dg[a], rg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], E, cX[a]);
                 m = fmax(m, E);
             }
         }
@@ -503,7 +504,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const int ck = (k == 0 ? cc[0] : k == 1 ? cc[1] : cc[2]) + sk;
             const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
             const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
-            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk);
+            const double rk = k == 0 ? rg[0] : k == 1 ? rg[1] : rg[2];
+            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk, rk);
             const bool bchg = (ck >> 3) != (k == 0 ? cb[0] : k == 1 ? cb[1] : cb[2]);
 #pragma unroll
             for (int a = 0; a < 3; ++a)
@@ -676,6 +678,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
             t_end = t1;
             t_in = -CUDART_INF;
+#if ARTEMIS_RCP_CROSSING
+#pragma unroll
+            for (int a = 0; a < 3; ++a) rg[a] = dg[a] != 0.0 ? __drcp_rn(dg[a]) : 0.0;
+#endif
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (dg[a] == 0.0) {
@@ -685,7 +691,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 } else {
                     cs[a] = dg[a] > 0.0 ? 1 : -1;
                     double E;
-                    sync_axis(og[a], dg[a], t0, aL[a], aU[a] - 1, cc[a], E, cX[a]);
+                    sync_axis(og[a], dg[a], rg[a], t0, aL[a], aU[a] - 1, cc[a], E, cX[a]);
                     t_in = fmax(t_in, E);
                 }
                 cb[a] = cc[a] >> 3;

@@ -11,6 +11,7 @@ VARIANTS = {
     "sout": ("ARTEMIS_STREAM_OUT=1",),
     "flat": ("ARTEMIS_FLAT_SHADE=1",),
     "nocull": ("ARTEMIS_CULL=0",),
+    "rcp": ("ARTEMIS_RCP_CROSSING=1",),
     "q4b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48", "ARTEMIS_MIN_BLOCKS=5"),
     "q4t40b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=40", "ARTEMIS_MIN_BLOCKS=5"),
     "q4t56b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=56", "ARTEMIS_MIN_BLOCKS=5"),
