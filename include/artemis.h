@@ -529,6 +529,12 @@ int artemis_host_widen_f32(const float *src /* host */, int64_t rows, int64_t co
                            int64_t src_pitch, double *dst /* host */, int64_t dst_pitch,
                            int threads);
 
+/* Test hook (no reference counterpart): n samples of the cell walk's
+ * reciprocal-corrected division against __ddiv_rn; the number of results
+ * that differ in any bit goes to *mismatches_host (must be 0). */
+int artemis_debug_division_selftest(int64_t n, uint64_t seed,
+                                    unsigned long long *mismatches_host);
+
 /* Synchronous device -> host copy (parity helpers). */
 int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);
 

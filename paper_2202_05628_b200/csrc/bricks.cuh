@@ -60,7 +60,7 @@ __device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick 
 #endif
 
 #ifndef ARTEMIS_RCP_CROSSING
-#define ARTEMIS_RCP_CROSSING 0
+#define ARTEMIS_RCP_CROSSING 1  // 0: __ddiv_rn per crossing (round 1; same results, slower)
 #endif
 // r = __drcp_rn(d), the correctly rounded reciprocal of the divisor (per ray,
 // per axis). With ARTEMIS_RCP_CROSSING the quotient is q = RN(n r) corrected

@@ -657,15 +657,19 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 aL[a] = __ldg(p.bm.aabb + a);
                 aU[a] = __ldg(p.bm.aabb + 3 + a);
             }
+#if ARTEMIS_RCP_CROSSING
+#pragma unroll
+            for (int a = 0; a < 3; ++a) rg[a] = dg[a] != 0.0 ? __drcp_rn(dg[a]) : 0.0;
+#endif
             double t0 = p.t_min, t1 = p.t_max;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const double lo = (double)aL[a], hi = (double)aU[a];
                 if (dg[a] == 0.0) {
                     if (og[a] < lo || og[a] >= hi) return;
-                } else {
-                    double ta = __ddiv_rn(__dadd_rn(lo, -og[a]), dg[a]);
-                    double tb = __ddiv_rn(__dadd_rn(hi, -og[a]), dg[a]);
+                } else {  // the slab test's exact plane distances (_core.pyx:252-285)
+                    double ta = crossing(aL[a], og[a], dg[a], rg[a]);
+                    double tb = crossing(aU[a], og[a], dg[a], rg[a]);
                     if (ta > tb) {
                         const double sw = ta;
                         ta = tb;
@@ -678,10 +682,6 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
             t_end = t1;
             t_in = -CUDART_INF;
-#if ARTEMIS_RCP_CROSSING
-#pragma unroll
-            for (int a = 0; a < 3; ++a) rg[a] = dg[a] != 0.0 ? __drcp_rn(dg[a]) : 0.0;
-#endif
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (dg[a] == 0.0) {
@@ -1398,6 +1398,93 @@ extern "C" int artemis_forward_fit(const artemis_tree_view *tree, const artemis_
         return launch_render_deg<kTrace, 0>(shade->degree, a,
                                                 ceil_div<int64_t>(rays->n_rays, 32), S(stream));
     });
+}
+
+// Self-test of the reciprocal-corrected division the cell walk uses
+// (bricks.cuh crossing): RN(q + (n - q d) r) with q = RN(n r), r = RN(1/d)
+// must equal __ddiv_rn(n, d) bit for bit. Samples per thread cycle through
+// regimes: walk-like (integer plane minus a grid-space origin over a grid
+// direction), divisors with all-ones or all-zeros significands (the
+// reciprocal's hardest cases), dividends one ulp off a divisor multiple,
+// and random bit patterns over a wide normal exponent range.
+__device__ __forceinline__ uint64_t splitmix(uint64_t &x) {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double rand_normal_bits(uint64_t &st, int emin, int emax) {
+    const uint64_t b = splitmix(st);
+    const int e = emin + (int)(splitmix(st) % (uint64_t)(emax - emin + 1));
+    const uint64_t bits = ((uint64_t)(e + 1023) << 52) | (b & 0x000FFFFFFFFFFFFFull) |
+                          (b & 0x8000000000000000ull);
+    return __longlong_as_double((long long)bits);
+}
+
+__global__ void division_selftest_kernel(int64_t n, uint64_t seed,
+                                         unsigned long long *mismatches) {
+    uint64_t st = seed ^ (0xD1B54A32D192ED03ull * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x));
+    unsigned long long bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double num, d;
+        switch (i & 3) {
+            case 0: {  // walk-like: k - o over a grid-space direction
+                const int k = (int)(splitmix(st) % 4096u) - 1024;
+                const double o = (double)(splitmix(st) >> 11) * 0x1.0p-53 * 4096.0 - 1024.0;
+                num = __dadd_rn((double)k, -o);
+                d = rand_normal_bits(st, -12, 12);
+                break;
+            }
+            case 1: {  // divisor significand all ones / all zeros
+                const int e = (int)(splitmix(st) % 41u) - 20;
+                const uint64_t mant = (splitmix(st) & 1) ? 0x000FFFFFFFFFFFFFull : 0ull;
+                d = __longlong_as_double((long long)(((uint64_t)(e + 1023) << 52) | mant));
+                if (splitmix(st) & 1) d = -d;
+                num = rand_normal_bits(st, -30, 30);
+                break;
+            }
+            case 2: {  // dividend one ulp off a multiple of the divisor
+                d = rand_normal_bits(st, -20, 20);
+                const double m = (double)(int64_t)(splitmix(st) % 100000u) - 50000.0;
+                const double x = __dmul_rn(m, d);
+                const int64_t step = (int64_t)(splitmix(st) % 3u) - 1;
+                num = __longlong_as_double(__double_as_longlong(x) + step);
+                break;
+            }
+            default:  // random patterns, wide normal range
+                num = rand_normal_bits(st, -400, 400);
+                d = rand_normal_bits(st, -400, 400);
+        }
+        if (d == 0.0 || !isfinite(num) || !isfinite(d)) continue;
+        const double r = __drcp_rn(d);
+        const double q = __dmul_rn(num, r);
+        const double fast = __fma_rn(__fma_rn(-q, d, num), r, q);
+        const double ref = __ddiv_rn(num, d);
+        if (__double_as_longlong(fast) != __double_as_longlong(ref) && !(isnan(fast) && isnan(ref)))
+            ++bad;
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+extern "C" int artemis_debug_division_selftest(int64_t n, uint64_t seed,
+                                               unsigned long long *mismatches_host) {
+    if (n < 0 || !mismatches_host) return ARTEMIS_ERR_ARG;
+    unsigned long long *d = nullptr;
+    ARTEMIS_TRY(cudaMalloc(&d, sizeof(*d)));
+    ARTEMIS_TRY(cudaMemset(d, 0, sizeof(*d)));
+    division_selftest_kernel<<<num_sms() * 8, 256>>>(n, seed, d);
+    int rc = ARTEMIS_LAUNCHED();
+    if (!rc) {
+        cudaError_t e = cudaMemcpy(mismatches_host, d, sizeof(*d), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            set_cuda_error(e);
+            rc = ARTEMIS_ERR_CUDA;
+        }
+    }
+    cudaFree(d);
+    return rc;
 }
 
 extern "C" int artemis_debug_set_render_blocks(int max_blocks) {

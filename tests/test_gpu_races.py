@@ -110,3 +110,18 @@ def test_sort_lookback_repeatable(bits):
     want = oracle.sort_order(keys)
     for _ in range(5):
         assert np.array_equal(K.sort_order(keys), want)
+
+
+def test_reciprocal_corrected_division_is_exact():
+    """The cell walk computes every plane crossing fl((k - o) / d) as
+    RN(q + (n - q d) r), q = RN(n r), r = RN(1/d) (bricks.cuh crossing);
+    Markstein's theorem makes that __ddiv_rn's result. 2^28 samples over
+    walk-like, adversarial-significand, near-multiple and wide random
+    operands must agree bit for bit (the config-scale trace digests in
+    test_gpu_traces.py pin it on the real walk)."""
+    import ctypes
+
+    L = _lib.lib()
+    bad = ctypes.c_ulonglong(0)
+    assert L.artemis_debug_division_selftest(1 << 28, 12345, ctypes.byref(bad)) == 0
+    assert bad.value == 0
