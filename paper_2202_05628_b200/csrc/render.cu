@@ -77,6 +77,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_STREAM_OUT
 #define ARTEMIS_STREAM_OUT 0  // 1: output maps stored evict-first (st.global.cs)
 #endif
+#ifndef ARTEMIS_FAST_CAMRAY
+#define ARTEMIS_FAST_CAMRAY 1  // camera rays with reciprocal-corrected divisions
+#endif
 #ifndef ARTEMIS_CULL
 #define ARTEMIS_CULL 0  // 1: fp32 AABB cull of camera rays (measured slower: DESIGN.md)
 #endif
@@ -307,6 +310,12 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     constexpr int H = (kDeg + 1) * (kDeg + 1);
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
+    __shared__ CamRecip s_camr[kCamera ? kMaxViews : 1];
+    if (kCamera) {
+        for (int v = threadIdx.x; v < (kMulti ? p.n_views : 1); v += blockDim.x)
+            s_camr[v] = camera_recip(p.cam[v]);
+        __syncthreads();
+    }
     using T0 = typename std::conditional<kRays == 1 || kRays == 3, float, double>::type;
     constexpr int kQueueBytes = queue_bytes(kRays == 1 || kRays == 3);
     constexpr int kStackB = stack_bytes(kDDA);
@@ -604,7 +613,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                         return;
                     }
                 }
+#if ARTEMIS_FAST_CAMRAY
+                camera_ray_fast(cam, s_camr[rv], px, py, og, dg, dw);
+#else
                 camera_ray(cam, px, py, og, dg, dw);
+#endif
             }
         } else {
             ray = id;

@@ -122,4 +122,53 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
     }
 }
 
+// RN(n / d) from r = RN(1/d): q = RN(n r) corrected once with the exact
+// residual (Markstein) -- bit-identical to __ddiv_rn(n, d), three fp64 ops
+// once the reciprocal is known (self-test: artemis_debug_division_selftest).
+__device__ __forceinline__ double div_rcp(double n, double d, double r) {
+    const double q = __dmul_rn(n, r);
+    return __fma_rn(__fma_rn(-q, d, n), r, q);
+}
+
+// Per-view constants of camera_ray_fast, computed once per block:
+// reciprocals of fx, fy and the cell size, and the grid-space origin.
+struct CamRecip {
+    double rfx, rfy, rcell[3], og[3];
+};
+
+__device__ __forceinline__ CamRecip camera_recip(const artemis_camera &c) {
+    CamRecip k;
+    k.rfx = __drcp_rn(c.fx);
+    k.rfy = __drcp_rn(c.fy);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        k.rcell[a] = __drcp_rn(c.cell[a]);
+        k.og[a] = __ddiv_rn(__dadd_rn(c.origin[a], -c.lo[a]), c.cell[a]);
+    }
+    return k;
+}
+
+// camera_ray with every division by a per-view constant (and the per-ray
+// norm) done as a reciprocal-corrected division: the same bits, shorter
+// dependent chains at ray start.
+__device__ __forceinline__ void camera_ray_fast(const artemis_camera &c, const CamRecip &k,
+                                                int u, int v, double og[3], double dg[3],
+                                                double dw[3]) {
+    const double c0 = div_rcp(__dadd_rn(__dadd_rn((double)u, 0.5), -c.cx), c.fx, k.rfx);
+    const double c1 = div_rcp(__dadd_rn(__dadd_rn((double)v, 0.5), -c.cy), c.fy, k.rfy);
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        d[a] = __fma_rn(1.0, c.R[3 * a + 2], __fma_rn(c1, c.R[3 * a + 1], __dmul_rn(c0, c.R[3 * a])));
+    const double nrm = __dsqrt_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+    const double rn = __drcp_rn(nrm);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        dw[a] = div_rcp(d[a], nrm, rn);
+        dg[a] = div_rcp(dw[a], c.cell[a], k.rcell[a]);
+        og[a] = k.og[a];
+    }
+}
+
 }  // namespace artemis
