@@ -533,7 +533,9 @@ int artemis_host_widen_f32(const float *src /* host */, int64_t rows, int64_t co
  * reciprocal-corrected division against __ddiv_rn; the number of results
  * that differ in any bit goes to *mismatches_host (must be 0). */
 int artemis_debug_division_selftest(int64_t n, uint64_t seed,
-                                    unsigned long long *mismatches_host);
+                                    unsigned long long *mismatches_host,
+                                    double *failed_host /* host, 48 doubles: first 16
+                                                           failures (regime, n, d); may be NULL */);
 
 /* Synchronous device -> host copy (parity helpers). */
 int artemis_copy_to_host(void *dst_host, const void *src_dev, size_t bytes, artemis_stream stream);

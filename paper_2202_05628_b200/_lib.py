@@ -141,7 +141,7 @@ _SIGS = {
     "artemis_host_checksum": (INT, [P, SZ, INT, P]),
     "artemis_host_widen_f32": (INT, [P, I64, I64, I64, P, I64, INT]),
     "artemis_debug_set_render_blocks": (INT, [INT]),
-    "artemis_debug_division_selftest": (INT, [I64, C.c_uint64, P]),
+    "artemis_debug_division_selftest": (INT, [I64, C.c_uint64, P, P]),
 }
 
 EXPORTS = tuple(_SIGS)

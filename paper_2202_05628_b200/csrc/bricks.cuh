@@ -62,17 +62,35 @@ __device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick 
 #ifndef ARTEMIS_RCP_CROSSING
 #define ARTEMIS_RCP_CROSSING 1  // 0: __ddiv_rn per crossing (round 1; same results, slower)
 #endif
-// r = __drcp_rn(d), the correctly rounded reciprocal of the divisor (per ray,
-// per axis). With ARTEMIS_RCP_CROSSING the quotient is q = RN(n r) corrected
-// once with the exact residual n - q d (one FMA): RN(q + (n - q d) r) is
-// RN(n / d) for a correctly rounded r (Markstein's theorem), i.e. exactly
-// __ddiv_rn's result, in three dependent fp64 ops.
+
+// RN(n / d) given r: with r = RN(1/d) != 0 and n, d, n/d far from under- and
+// overflow, q = RN(n r) corrected once with the exact residual n - q d,
+// RN(q + (n - q d) r), is RN(n / d) (Markstein) -- __ddiv_rn's bits in three
+// dependent fp64 ops; anything else (r == 0 marks an out-of-range divisor,
+// |n| outside [2^-400, 2^400] and not 0) takes __ddiv_rn. The GPU self-test
+// (artemis_debug_division_selftest, with subnormal and extreme operands)
+// checks it against __ddiv_rn bit for bit.
+__device__ __forceinline__ double div_exact(double n, double d, double r) {
+    const double an = fabs(n);
+    if (r != 0.0 && ((an >= 0x1p-400 && an <= 0x1p400) || n == 0.0)) {
+        const double q = __dmul_rn(n, r);
+        return __fma_rn(__fma_rn(-q, d, n), r, q);
+    }
+    return __ddiv_rn(n, d);
+}
+
+// the divisor's reciprocal for div_exact (0 = out of the fast path's range)
+__device__ __forceinline__ double recip_for_div(double d) {
+    const double ad = fabs(d);
+    return (ad >= 0x1p-400 && ad <= 0x1p400) ? __drcp_rn(d) : 0.0;
+}
+
+// Exact plane crossing fl((k - o) / d) -- the same double the reference's
+// slab test computes for the plane k of a unit cell; r = recip_for_div(d).
 __device__ __forceinline__ double crossing(int k, double o, double d, double r) {
     ARTEMIS_STAT(0);
 #if ARTEMIS_RCP_CROSSING
-    const double n = __dadd_rn((double)k, -o);
-    const double q = __dmul_rn(n, r);
-    return __fma_rn(__fma_rn(-q, d, n), r, q);
+    return div_exact(__dadd_rn((double)k, -o), d, r);
 #else
     (void)r;
     return __ddiv_rn(__dadd_rn((double)k, -o), d);

@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
 #if ARTEMIS_RCP_CROSSING
 #pragma unroll
-            for (int a = 0; a < 3; ++a) rg[a] = dg[a] != 0.0 ? __drcp_rn(dg[a]) : 0.0;
+            for (int a = 0; a < 3; ++a) rg[a] = recip_for_div(dg[a]);
 #endif
             double t0 = p.t_min, t1 = p.t_max;
 #pragma unroll
@@ -1436,7 +1436,7 @@ __device__ __forceinline__ double rand_normal_bits(uint64_t &st, int emin, int e
 }
 
 __global__ void division_selftest_kernel(int64_t n, uint64_t seed,
-                                         unsigned long long *mismatches) {
+                                         unsigned long long *mismatches, double *failed) {
     uint64_t st = seed ^ (0xD1B54A32D192ED03ull * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x));
     unsigned long long bad = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1471,24 +1471,38 @@ __global__ void division_selftest_kernel(int64_t n, uint64_t seed,
                 d = rand_normal_bits(st, -400, 400);
         }
         if (d == 0.0 || !isfinite(num) || !isfinite(d)) continue;
-        const double r = __drcp_rn(d);
-        const double q = __dmul_rn(num, r);
-        const double fast = __fma_rn(__fma_rn(-q, d, num), r, q);
+        const double fast = div_exact(num, d, recip_for_div(d));  // what the walk runs
         const double ref = __ddiv_rn(num, d);
-        if (__double_as_longlong(fast) != __double_as_longlong(ref) && !(isnan(fast) && isnan(ref)))
+        if (__double_as_longlong(fast) != __double_as_longlong(ref) && !(isnan(fast) && isnan(ref))) {
             ++bad;
+            if (failed) {  // record a few (regime, n, d) for diagnosis
+                const unsigned long long slot = atomicAdd(mismatches + 1, 1ull);
+                if (slot < 16) {
+                    failed[3 * slot] = (double)(i & 3);
+                    failed[3 * slot + 1] = num;
+                    failed[3 * slot + 2] = d;
+                }
+            }
+        }
     }
     if (bad) atomicAdd(mismatches, bad);
 }
 
 extern "C" int artemis_debug_division_selftest(int64_t n, uint64_t seed,
-                                               unsigned long long *mismatches_host) {
+                                               unsigned long long *mismatches_host,
+                                               double *failed_host /* 48 doubles, may be NULL */) {
     if (n < 0 || !mismatches_host) return ARTEMIS_ERR_ARG;
     unsigned long long *d = nullptr;
-    ARTEMIS_TRY(cudaMalloc(&d, sizeof(*d)));
-    ARTEMIS_TRY(cudaMemset(d, 0, sizeof(*d)));
-    division_selftest_kernel<<<num_sms() * 8, 256>>>(n, seed, d);
+    double *fd = nullptr;
+    ARTEMIS_TRY(cudaMalloc(&d, 2 * sizeof(*d)));
+    ARTEMIS_TRY(cudaMemset(d, 0, 2 * sizeof(*d)));
+    ARTEMIS_TRY(cudaMalloc(&fd, 48 * sizeof(double)));
+    ARTEMIS_TRY(cudaMemset(fd, 0, 48 * sizeof(double)));
+    division_selftest_kernel<<<num_sms() * 8, 256>>>(n, seed, d, fd);
     int rc = ARTEMIS_LAUNCHED();
+    if (!rc && failed_host)
+        cudaMemcpy(failed_host, fd, 48 * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(fd);
     if (!rc) {
         cudaError_t e = cudaMemcpy(mismatches_host, d, sizeof(*d), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) {

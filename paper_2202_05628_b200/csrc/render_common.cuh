@@ -122,13 +122,9 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
     }
 }
 
-// RN(n / d) from r = RN(1/d): q = RN(n r) corrected once with the exact
-// residual (Markstein) -- bit-identical to __ddiv_rn(n, d), three fp64 ops
-// once the reciprocal is known (self-test: artemis_debug_division_selftest).
-__device__ __forceinline__ double div_rcp(double n, double d, double r) {
-    const double q = __dmul_rn(n, r);
-    return __fma_rn(__fma_rn(-q, d, n), r, q);
-}
+// RN(n / d) from r = recip_for_div(d) (bricks.cuh div_exact: Markstein's
+// corrected reciprocal, __ddiv_rn outside its safe range)
+__device__ __forceinline__ double div_rcp(double n, double d, double r) { return div_exact(n, d, r); }
 
 // Per-view constants of camera_ray_fast, computed once per block:
 // reciprocals of fx, fy and the cell size, and the grid-space origin.
@@ -138,11 +134,11 @@ struct CamRecip {
 
 __device__ __forceinline__ CamRecip camera_recip(const artemis_camera &c) {
     CamRecip k;
-    k.rfx = __drcp_rn(c.fx);
-    k.rfy = __drcp_rn(c.fy);
+    k.rfx = recip_for_div(c.fx);
+    k.rfy = recip_for_div(c.fy);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        k.rcell[a] = __drcp_rn(c.cell[a]);
+        k.rcell[a] = recip_for_div(c.cell[a]);
         k.og[a] = __ddiv_rn(__dadd_rn(c.origin[a], -c.lo[a]), c.cell[a]);
     }
     return k;
@@ -162,7 +158,7 @@ __device__ __forceinline__ void camera_ray_fast(const artemis_camera &c, const C
         d[a] = __fma_rn(1.0, c.R[3 * a + 2], __fma_rn(c1, c.R[3 * a + 1], __dmul_rn(c0, c.R[3 * a])));
     const double nrm = __dsqrt_rn(
         __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
-    const double rn = __drcp_rn(nrm);
+    const double rn = recip_for_div(nrm);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         dw[a] = div_rcp(d[a], nrm, rn);

@@ -12,6 +12,9 @@
 //   rotation joint = joint of the first maximal weight slot
 // One thread per voxel; the per-joint 3x4 blocks sit in shared memory; the
 // K = 4 slot rows are read as one int4 and two double2.
+#include <cmath>
+
+#include "bricks.cuh"
 #include "common.cuh"
 #include "tree.cuh"
 
@@ -31,6 +34,7 @@ struct WarpArgs {
     const double *aff;    // (J, 12)
     int n_joints;
     double lo[3], cell[3];
+    double rcell[3];      // RN(1 / cell): the floor's division as div_rcp (bit-identical)
     int res;
     // API outputs
     double *positions;
@@ -102,7 +106,8 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
             ok = true;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                double f = floor(__ddiv_rn(__dadd_rn(p[k], -a.lo[k]), a.cell[k]));
+                // RN((p - lo) / cell) via the cell's reciprocal (div_exact: exact)
+                double f = floor(div_exact(__dadd_rn(p[k], -a.lo[k]), a.cell[k], a.rcell[k]));
                 // NaN and out-of-range both fail this test, like the reference's
                 // int64 cast + range check (rigging.py:369-371)
                 if (!(f >= 0.0 && f < (double)a.res)) ok = false;
@@ -178,6 +183,8 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
     for (int k = 0; k < 3; ++k) {
         a.lo[k] = lo[k];
         a.cell[k] = cell[k];
+        // IEEE double division (correctly rounded); 0 leaves div_exact on __ddiv_rn
+        a.rcell[k] = (std::fabs(cell[k]) >= 0x1p-400 && std::fabs(cell[k]) <= 0x1p400) ? 1.0 / cell[k] : 0.0;
     }
     a.res = res;
     a.keys = keys;
@@ -216,6 +223,8 @@ extern "C" int artemis_warp(const int32_t *cells, int64_t n, int slots, const in
     for (int k = 0; k < 3; ++k) {
         a.lo[k] = lo[k];
         a.cell[k] = cell[k];
+        // IEEE double division (correctly rounded); 0 leaves div_exact on __ddiv_rn
+        a.rcell[k] = (std::fabs(cell[k]) >= 0x1p-400 && std::fabs(cell[k]) <= 0x1p400) ? 1.0 / cell[k] : 0.0;
     }
     a.res = resolution;
     a.positions = positions;
