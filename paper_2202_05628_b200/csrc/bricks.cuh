@@ -63,30 +63,40 @@ __device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick 
 #define ARTEMIS_RCP_CROSSING 1  // 0: __ddiv_rn per crossing (round 1; same results, slower)
 #endif
 
-// RN(n / d) given r: with r = RN(1/d) != 0 and n, d, n/d far from under- and
-// overflow, q = RN(n r) corrected once with the exact residual n - q d,
-// RN(q + (n - q d) r), is RN(n / d) (Markstein) -- __ddiv_rn's bits in three
-// dependent fp64 ops; anything else (r == 0 marks an out-of-range divisor,
-// |n| outside [2^-400, 2^400] and not 0) takes __ddiv_rn. The GPU self-test
-// (artemis_debug_division_selftest, with subnormal and extreme operands)
-// checks it against __ddiv_rn bit for bit.
+// RN(n / d). Markstein: with r = RN(1/d) and n, d, n/d well inside the
+// normal range, q = RN(n r) corrected once with the exact residual n - q d,
+// RN(q + (n - q d) r), is RN(n / d) -- __ddiv_rn's bits in three dependent
+// fp64 ops. Outside that range it can differ (a subnormal dividend did, in
+// the GPU self-test), so the range is established by the CALLER, once per
+// divisor: r != 0 asserts that every dividend it will see is 0 or has
+// magnitude in [2^-400, 2^400] and that |d| is in [2^-400, 2^400]; r == 0
+// takes __ddiv_rn (out of line: it never runs on real rays).
+static __device__ __noinline__ double div_slow(double n, double d) { return __ddiv_rn(n, d); }
+
 __device__ __forceinline__ double div_exact(double n, double d, double r) {
-    const double an = fabs(n);
-    if (r != 0.0 && ((an >= 0x1p-400 && an <= 0x1p400) || n == 0.0)) {
+    if (r != 0.0) {
         const double q = __dmul_rn(n, r);
         return __fma_rn(__fma_rn(-q, d, n), r, q);
     }
-    return __ddiv_rn(n, d);
+    return div_slow(n, d);
 }
 
-// the divisor's reciprocal for div_exact (0 = out of the fast path's range)
+// r for div_exact when every dividend is known to be 0 or in [2^-400, 2^400]
 __device__ __forceinline__ double recip_for_div(double d) {
     const double ad = fabs(d);
     return (ad >= 0x1p-400 && ad <= 0x1p400) ? __drcp_rn(d) : 0.0;
 }
 
+// r for the plane crossings of one ray axis: dividends k - o with integer
+// |k| <= 2^22 are 0 or in [2^-353, 2^301] whenever o is 0 or |o| is in
+// [2^-300, 2^300] (a nonzero k - o is a multiple of ulp(o) > 2^-353)
+__device__ __forceinline__ double recip_for_crossings(double o, double d) {
+    const double ao = fabs(o);
+    return (o == 0.0 || (ao >= 0x1p-300 && ao <= 0x1p300)) ? recip_for_div(d) : 0.0;
+}
+
 // Exact plane crossing fl((k - o) / d) -- the same double the reference's
-// slab test computes for the plane k of a unit cell; r = recip_for_div(d).
+// slab test computes for the plane k of a unit cell; r = recip_for_crossings.
 __device__ __forceinline__ double crossing(int k, double o, double d, double r) {
     ARTEMIS_STAT(0);
 #if ARTEMIS_RCP_CROSSING

@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             }
 #if ARTEMIS_RCP_CROSSING
 #pragma unroll
-            for (int a = 0; a < 3; ++a) rg[a] = recip_for_div(dg[a]);
+            for (int a = 0; a < 3; ++a) rg[a] = recip_for_crossings(og[a], dg[a]);
 #endif
             double t0 = p.t_min, t1 = p.t_max;
 #pragma unroll
@@ -1471,7 +1471,9 @@ __global__ void division_selftest_kernel(int64_t n, uint64_t seed,
                 d = rand_normal_bits(st, -400, 400);
         }
         if (d == 0.0 || !isfinite(num) || !isfinite(d)) continue;
-        const double fast = div_exact(num, d, recip_for_div(d));  // what the walk runs
+        const double an = fabs(num);  // div_exact's contract: the caller vouches for the dividend
+        const double r = (num == 0.0 || (an >= 0x1p-400 && an <= 0x1p400)) ? recip_for_div(d) : 0.0;
+        const double fast = div_exact(num, d, r);
         const double ref = __ddiv_rn(num, d);
         if (__double_as_longlong(fast) != __double_as_longlong(ref) && !(isnan(fast) && isnan(ref))) {
             ++bad;

@@ -122,10 +122,6 @@ __device__ __forceinline__ void camera_ray(const artemis_camera &c, int u, int v
     }
 }
 
-// RN(n / d) from r = recip_for_div(d) (bricks.cuh div_exact: Markstein's
-// corrected reciprocal, __ddiv_rn outside its safe range)
-__device__ __forceinline__ double div_rcp(double n, double d, double r) { return div_exact(n, d, r); }
-
 // Per-view constants of camera_ray_fast, computed once per block:
 // reciprocals of fx, fy and the cell size, and the grid-space origin.
 struct CamRecip {
@@ -146,12 +142,27 @@ __device__ __forceinline__ CamRecip camera_recip(const artemis_camera &c) {
 
 // camera_ray with every division by a per-view constant (and the per-ray
 // norm) done as a reciprocal-corrected division: the same bits, shorter
-// dependent chains at ray start.
+// dependent chains at ray start. Dividends: (u + 0.5) - cx is 0 or >= 2^-53
+// |cx| in magnitude for any sane principal point, d[a] and dw[a] are 0 or
+// >= ~1e-17 for rotations away from underflow; a ray with an operand outside
+// div_exact's range falls back to camera_ray (checked here, never taken on
+// real cameras).
+__device__ __forceinline__ bool div_ok(double n) {
+    const double an = fabs(n);
+    return n == 0.0 || (an >= 0x1p-400 && an <= 0x1p400);
+}
+
 __device__ __forceinline__ void camera_ray_fast(const artemis_camera &c, const CamRecip &k,
                                                 int u, int v, double og[3], double dg[3],
                                                 double dw[3]) {
-    const double c0 = div_rcp(__dadd_rn(__dadd_rn((double)u, 0.5), -c.cx), c.fx, k.rfx);
-    const double c1 = div_rcp(__dadd_rn(__dadd_rn((double)v, 0.5), -c.cy), c.fy, k.rfy);
+    const double n0 = __dadd_rn(__dadd_rn((double)u, 0.5), -c.cx);
+    const double n1 = __dadd_rn(__dadd_rn((double)v, 0.5), -c.cy);
+    if (k.rfx == 0.0 || k.rfy == 0.0 || !div_ok(n0) || !div_ok(n1)) {
+        camera_ray(c, u, v, og, dg, dw);
+        return;
+    }
+    const double c0 = div_exact(n0, c.fx, k.rfx);
+    const double c1 = div_exact(n1, c.fy, k.rfy);
     double d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
@@ -159,10 +170,16 @@ __device__ __forceinline__ void camera_ray_fast(const artemis_camera &c, const C
     const double nrm = __dsqrt_rn(
         __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
     const double rn = recip_for_div(nrm);
+    if (rn == 0.0 || !div_ok(d[0]) || !div_ok(d[1]) || !div_ok(d[2])) {
+        camera_ray(c, u, v, og, dg, dw);
+        return;
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        dw[a] = div_rcp(d[a], nrm, rn);
-        dg[a] = div_rcp(dw[a], c.cell[a], k.rcell[a]);
+        dw[a] = div_exact(d[a], nrm, rn);
+        // |dw| <= 1 and 0 or >= |d[a]| / nrm: in range; the cell reciprocal
+        // is 0 (-> __ddiv_rn) for an out-of-range cell size
+        dg[a] = div_ok(dw[a]) ? div_exact(dw[a], c.cell[a], k.rcell[a]) : __ddiv_rn(dw[a], c.cell[a]);
         og[a] = k.og[a];
     }
 }

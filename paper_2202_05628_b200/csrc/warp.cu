@@ -34,7 +34,7 @@ struct WarpArgs {
     const double *aff;    // (J, 12)
     int n_joints;
     double lo[3], cell[3];
-    double rcell[3];      // RN(1 / cell): the floor's division as div_rcp (bit-identical)
+    double rcell[3];      // RN(1 / cell): the floor division as div_exact (bit-identical)
     int res;
     // API outputs
     double *positions;
@@ -106,8 +106,12 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
             ok = true;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                // RN((p - lo) / cell) via the cell's reciprocal (div_exact: exact)
-                double f = floor(div_exact(__dadd_rn(p[k], -a.lo[k]), a.cell[k], a.rcell[k]));
+                // RN((p - lo) / cell) via the cell's reciprocal (div_exact: exact
+                // when the dividend is in range; else __ddiv_rn)
+                const double n = __dadd_rn(p[k], -a.lo[k]);
+                const double an = fabs(n);
+                const bool ok_n = n == 0.0 || (an >= 0x1p-400 && an <= 0x1p400);
+                double f = floor(div_exact(n, a.cell[k], ok_n ? a.rcell[k] : 0.0));
                 // NaN and out-of-range both fail this test, like the reference's
                 // int64 cast + range check (rigging.py:369-371)
                 if (!(f >= 0.0 && f < (double)a.res)) ok = false;

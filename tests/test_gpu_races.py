@@ -123,5 +123,5 @@ def test_reciprocal_corrected_division_is_exact():
 
     L = _lib.lib()
     bad = ctypes.c_ulonglong(0)
-    assert L.artemis_debug_division_selftest(1 << 28, 12345, ctypes.byref(bad)) == 0
+    assert L.artemis_debug_division_selftest(1 << 28, 12345, ctypes.byref(bad), None) == 0
     assert bad.value == 0
