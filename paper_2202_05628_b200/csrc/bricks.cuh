@@ -60,85 +60,89 @@ __device__ unsigned long long g_walk_stats[4];  // crossings, cell steps, brick 
 #endif
 
 #ifndef ARTEMIS_RCP_CROSSING
-#define ARTEMIS_RCP_CROSSING 1  // 0: __ddiv_rn per crossing (round 1; same results, slower)
+#define ARTEMIS_RCP_CROSSING 1  // 0: __ddiv_rn for every crossing (round 1; same results, slower)
 #endif
 
-// RN(n / d). Markstein: with r = RN(1/d) and n, d, n/d well inside the
-// normal range, q = RN(n r) corrected once with the exact residual n - q d,
-// RN(q + (n - q d) r), is RN(n / d) -- __ddiv_rn's bits in three dependent
-// fp64 ops. Outside that range it can differ (a subnormal dividend did, in
-// the GPU self-test), so the range is established by the CALLER, once per
-// divisor: r != 0 asserts that every dividend it will see is 0 or has
-// magnitude in [2^-400, 2^400] and that |d| is in [2^-400, 2^400]; r == 0
-// takes __ddiv_rn (out of line: it never runs on real rays).
+// RN(n / d) from r = RN(1/d) (Markstein): q = RN(n r) corrected once with
+// the exact residual n - q d, RN(q + (n - q d) r), equals RN(n / d) --
+// __ddiv_rn's bits in three dependent fp64 ops -- as long as nothing
+// underflows or overflows (n, d, n / d well inside the normal range). The
+// GPU self-test (artemis_debug_division_selftest) found the failure mode
+// outside it: a subnormal dividend. div_fast is used where the caller has
+// established the operand ranges for the whole launch (camera frames:
+// camera_fast_div_ok in frame.cu); div_exact checks per call.
+__device__ __forceinline__ double div_fast(double n, double d, double r) {
+    const double q = __dmul_rn(n, r);
+    return __fma_rn(__fma_rn(-q, d, n), r, q);
+}
+
 static __device__ __noinline__ double div_slow(double n, double d) { return __ddiv_rn(n, d); }
 
+// safe-range predicate of div_fast's operands (0 is always fine)
+__device__ __forceinline__ bool div_operand_ok(double x, double lo, double hi) {
+    const double a = fabs(x);
+    return x == 0.0 || (a >= lo && a <= hi);
+}
+
 __device__ __forceinline__ double div_exact(double n, double d, double r) {
-    if (r != 0.0) {
-        const double q = __dmul_rn(n, r);
-        return __fma_rn(__fma_rn(-q, d, n), r, q);
-    }
+    if (r != 0.0 && div_operand_ok(n, 0x1p-400, 0x1p400)) return div_fast(n, d, r);
     return div_slow(n, d);
 }
 
-// r for div_exact when every dividend is known to be 0 or in [2^-400, 2^400]
+// r for div_exact / div_fast (0 = divisor out of range: div_exact falls back)
 __device__ __forceinline__ double recip_for_div(double d) {
     const double ad = fabs(d);
-    return (ad >= 0x1p-400 && ad <= 0x1p400) ? __drcp_rn(d) : 0.0;
-}
-
-// r for the plane crossings of one ray axis: dividends k - o with integer
-// |k| <= 2^22 are 0 or in [2^-353, 2^301] whenever o is 0 or |o| is in
-// [2^-300, 2^300] (a nonzero k - o is a multiple of ulp(o) > 2^-353)
-__device__ __forceinline__ double recip_for_crossings(double o, double d) {
-    const double ao = fabs(o);
-    return (o == 0.0 || (ao >= 0x1p-300 && ao <= 0x1p300)) ? recip_for_div(d) : 0.0;
+    return (ad >= 0x1p-600 && ad <= 0x1p600) ? __drcp_rn(d) : 0.0;
 }
 
 // Exact plane crossing fl((k - o) / d) -- the same double the reference's
-// slab test computes for the plane k of a unit cell; r = recip_for_crossings.
+// slab test computes for the plane k of a unit cell. kFast: the launch's
+// operand ranges are established (k - o is 0 or in [2^-353, 2^301], d in
+// [2^-487, 2^60]: every quotient, product and residual normal), r = RN(1/d).
+template <bool kFast>
 __device__ __forceinline__ double crossing(int k, double o, double d, double r) {
     ARTEMIS_STAT(0);
-#if ARTEMIS_RCP_CROSSING
-    return div_exact(__dadd_rn((double)k, -o), d, r);
-#else
-    (void)r;
-    return __ddiv_rn(__dadd_rn((double)k, -o), d);
-#endif
+    if constexpr (kFast) {
+        return div_fast(__dadd_rn((double)k, -o), d, r);
+    } else {
+        (void)r;
+        return __ddiv_rn(__dadd_rn((double)k, -o), d);
+    }
 }
 
 // Slab of one axis that contains distance t (entry <= t < exit), searched
 // from an estimate inside [cmin, cmax]; returns its exact entry/exit.
+template <bool kFast>
 __device__ __forceinline__ void sync_axis(double o, double d, double r, double t, int cmin,
                                           int cmax, int &c, double &E, double &X) {
     ARTEMIS_STAT(3);
     const double est = floor(o + t * d);
     c = est < (double)cmin ? cmin : est > (double)cmax ? cmax : (int)est;
     if (d > 0.0) {  // slab c = [cross(c), cross(c+1))
-        double lo = crossing(c, o, d, r);
+        double lo = crossing<kFast>(c, o, d, r);
         while (c > cmin && lo > t) {
             --c;
-            lo = crossing(c, o, d, r);
+            lo = crossing<kFast>(c, o, d, r);
         }
-        double hi = crossing(c + 1, o, d, r);
+        double hi = crossing<kFast>(c + 1, o, d, r);
         while (c < cmax && hi <= t) {
             ++c;
             lo = hi;
-            hi = crossing(c + 1, o, d, r);
+            hi = crossing<kFast>(c + 1, o, d, r);
         }
         E = lo;
         X = hi;
     } else {  // slab c = [cross(c+1), cross(c))
-        double en = crossing(c + 1, o, d, r);
+        double en = crossing<kFast>(c + 1, o, d, r);
         while (c < cmax && en > t) {
             ++c;
-            en = crossing(c + 1, o, d, r);
+            en = crossing<kFast>(c + 1, o, d, r);
         }
-        double ex = crossing(c, o, d, r);
+        double ex = crossing<kFast>(c, o, d, r);
         while (c > cmin && ex <= t) {
             --c;
             en = ex;
-            ex = crossing(c, o, d, r);
+            ex = crossing<kFast>(c, o, d, r);
         }
         E = en;
         X = ex;

@@ -51,7 +51,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
                   float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
-                  int outputs_ready, cudaStream_t st);
+                  int outputs_ready, int fast_div, cudaStream_t st);
 int render_clear_outputs(float *F, void *A, void *D, int64_t n, int channels, int sharded,
                          int maps64, cudaStream_t st);
 
@@ -116,7 +116,7 @@ struct artemis_frame_s {
     // without re-capturing
     struct GraphSlot {
         cudaGraphExec_t exec = nullptr;
-        int w = 0, h = 0, flags = 0, identity = -1, nj = 0, sharded = 0;
+        int w = 0, h = 0, flags = 0, identity = -1, nj = 0, sharded = 0, fast_div = -1;
         const void *F = nullptr, *A = nullptr, *D = nullptr;
         cudaStream_t stream = nullptr;
         double lambda = 0, sigma_dep = 0;
@@ -153,6 +153,7 @@ struct artemis_frame_s {
     void *peer_out[3] = {nullptr, nullptr, nullptr};
     int64_t peer_pixels = 0;  // size of the peer maps (pixels) and their alpha/depth type
     int peer_maps64 = 0;
+    int fast_div = 0;  // this run's cameras are in div_fast's operand ranges
     int profile = 0;
 };
 
@@ -231,7 +232,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, f->n, 0, st);
+                           vo.D, f->n, 0, f->fast_div, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -340,7 +341,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                sigma_dep, flags & 1, (flags & 8) ? 1 : 0, vo.F[v], vo.A[v],
                                vo.D[v], reinterpret_cast<unsigned long long *>(f->counters + 2),
                                order, &f->params->order_on, nullptr, 1, nullptr, nullptr, nullptr,
-                               f->n, 1, st);
+                               f->n, 1, f->fast_div, st);
         }
         launches += vo.n - 1;
     } else {
@@ -348,7 +349,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, f->n, 1, st);
+                           vo.D, f->n, 1, f->fast_div, st);
     }
     mark(5);
     launches += 1;
@@ -625,6 +626,37 @@ static int run_frame_launch(artemis_frame f, int identity, int n_joints, const a
 // One posed frame: warp + rebuild once, then one render launch over the
 // views cam[0 .. vo.n) (the outputs of view v in vo, or F/alpha/depth for a
 // single view).
+// Whether every plane crossing and camera-ray division of frames seen
+// through this camera stays inside div_fast's exact range (bricks.cuh):
+// positive focal lengths in [2^-20, 2^60], principal point, rotation entries
+// and grid-space origin each 0 or of magnitude in [2^-300, 2^300] (rotation
+// entries at most 2), cell sizes in [2^-60, 2^60]. Then (u + 0.5) - cx is 0
+// or >= 2^-353, every ray-direction component is 0 or >= 2^-427 with the
+// norm >= 1, |k - og| is 0 or in [2^-353, 2^301] for the grid planes k
+// (|k| <= 2^22), grid directions are 0 or in [2^-487, 2^60]: all quotients,
+// products and residuals normal. Otherwise the launch takes __ddiv_rn (same
+// bits, slower).
+static bool in_range_or_zero(double x, double lo, double hi) {
+    const double a = fabs(x);
+    return x == 0.0 || (a >= lo && a <= hi);
+}
+
+static bool camera_fast_div_ok(const artemis_camera &c) {
+    const char *env = getenv("ARTEMIS_FAST_DIV");  // "0": always __ddiv_rn (A/B, tests)
+    if (env && env[0] == '0') return false;
+    if (!(c.fx >= 0x1p-20 && c.fx <= 0x1p60 && c.fy >= 0x1p-20 && c.fy <= 0x1p60)) return false;
+    if (!in_range_or_zero(c.cx, 0x1p-300, 0x1p300) || !in_range_or_zero(c.cy, 0x1p-300, 0x1p300))
+        return false;
+    for (int i = 0; i < 9; ++i)
+        if (!in_range_or_zero(c.R[i], 0x1p-300, 2.0)) return false;
+    for (int a = 0; a < 3; ++a) {
+        if (!(c.cell[a] >= 0x1p-60 && c.cell[a] <= 0x1p60)) return false;
+        const double og = (c.origin[a] - c.lo[a]) / c.cell[a];  // = the device's __ddiv_rn value
+        if (!in_range_or_zero(og, 0x1p-300, 0x1p300)) return false;
+    }
+    return true;
+}
+
 static int frame_run_impl(artemis_frame f, const double *joint_aff, const double *rot_inv,
                           int n_joints, const artemis_camera *cam, double lambda_th,
                           double sigma_dep, int flags, float *F, void *alpha, void *depth,
@@ -679,6 +711,9 @@ static int frame_run_impl(artemis_frame f, const double *joint_aff, const double
     ARTEMIS_TRY(cudaMemcpyAsync(&f->params->order_on, &hp->order_on, sizeof(int32_t),
                                 cudaMemcpyHostToDevice, st));
     ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));  // the staging block may be reused after this
+    f->fast_div = 1;
+    for (int v = 0; v < vo.n; ++v)
+        if (!camera_fast_div_ok(cam[v])) f->fast_div = 0;
     return run_frame_launch(f, identity, n_joints, cam, sharded, lambda_th, sigma_dep, flags, F,
                             alpha, depth, order, vo, st);
 }
@@ -725,7 +760,8 @@ static int run_frame_launch(artemis_frame f, int identity, int n_joints, const a
         if (g.exec && g.w == cam->width && g.h == cam->height && g.flags == flags &&
             g.identity == identity && g.nj == n_joints && g.F == F && g.A == alpha &&
             g.D == depth && g.stream == st && g.lambda == lambda_th &&
-            g.sigma_dep == sigma_dep && g.sharded == sharded && same_views(g.views, vo)) {
+            g.sigma_dep == sigma_dep && g.sharded == sharded && g.fast_div == f->fast_div &&
+            same_views(g.views, vo)) {
             slot = &g;
             break;
         }
@@ -769,6 +805,7 @@ static int run_frame_launch(artemis_frame f, int identity, int n_joints, const a
         slot->lambda = lambda_th;
         slot->sigma_dep = sigma_dep;
         slot->sharded = sharded;
+        slot->fast_div = f->fast_div;
         slot->views = vo;
     }
     slot->used = ++f->graph_clock;

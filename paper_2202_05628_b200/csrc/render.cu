@@ -303,7 +303,7 @@ __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t 
 // kRays: 0 = explicit ray arrays (fp64 maps), 1 = in-kernel camera rays with
 // fp32 alpha/depth maps (frame pipeline), 2 = camera rays with fp64 maps,
 // 3 / 4 = as 1 / 2 over several views in one launch (run_views)
-template <int kDeg, int kMode, int kRays, bool kVec, bool kDDA>
+template <int kDeg, int kMode, int kRays, bool kVec, bool kDDA, bool kFast>
 __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_kernel(RenderArgs p) {
     constexpr bool kCamera = kRays != 0;
     constexpr bool kMulti = kRays >= 3;  // several views per launch (run_views)
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     extern __shared__ __align__(16) unsigned char s_raw[];
     int *s_stack = reinterpret_cast<int *>(s_raw);
     __shared__ CamRecip s_camr[kCamera ? kMaxViews : 1];
-    if (kCamera) {
+    if (kCamera && kFast) {
         for (int v = threadIdx.x; v < (kMulti ? p.n_views : 1); v += blockDim.x)
             s_camr[v] = camera_recip(p.cam[v]);
         __syncthreads();
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // while inside an occupied brick. Empty bricks cost one crossing each;
     // entering an occupied brick re-derives the other axes' cells there.
     auto brick_exit = [&](int a) {  // exact crossing of the current brick's exit plane on axis a
-        return cs[a] != 0 ? crossing(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a], rg[a])
+        return cs[a] != 0 ? crossing<kFast>(cs[a] > 0 ? (cb[a] + 1) * 8 : cb[a] * 8, og[a], dg[a], rg[a])
                           : CUDART_INF;
     };
     auto enter_brick = [&](unsigned advanced, double tn) {
@@ -456,10 +456,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 const int cn = cs[a] > 0 ? cb[a] * 8 : cb[a] * 8 + 7;
                 cc[a] = cn;
                 m = fmax(m, tn);
-                cX[a] = crossing(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a], rg[a]);
+                cX[a] = crossing<kFast>(cs[a] > 0 ? cn + 1 : cn, og[a], dg[a], rg[a]);
             } else {
                 double E;
-                sync_axis(og[a], dg[a], rg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], E, cX[a]);
+                sync_axis<kFast>(og[a], dg[a], rg[a], tn, cb[a] * 8, cb[a] * 8 + 7, cc[a], E, cX[a]);
                 m = fmax(m, E);
             }
         }
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const double ok = k == 0 ? og[0] : k == 1 ? og[1] : og[2];
             const double dk = k == 0 ? dg[0] : k == 1 ? dg[1] : dg[2];
             const double rk = k == 0 ? rg[0] : k == 1 ? rg[1] : rg[2];
-            const double xn = crossing(sk > 0 ? ck + 1 : ck, ok, dk, rk);
+            const double xn = crossing<kFast>(sk > 0 ? ck + 1 : ck, ok, dk, rk);
             const bool bchg = (ck >> 3) != (k == 0 ? cb[0] : k == 1 ? cb[1] : cb[2]);
 #pragma unroll
             for (int a = 0; a < 3; ++a)
@@ -613,11 +613,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                         return;
                     }
                 }
-#if ARTEMIS_FAST_CAMRAY
-                camera_ray_fast(cam, s_camr[rv], px, py, og, dg, dw);
-#else
-                camera_ray(cam, px, py, og, dg, dw);
-#endif
+                if constexpr (kFast && ARTEMIS_FAST_CAMRAY)
+                    camera_ray_fast(cam, s_camr[rv], px, py, og, dg, dw);
+                else
+                    camera_ray(cam, px, py, og, dg, dw);
             }
         } else {
             ray = id;
@@ -670,10 +669,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 aL[a] = __ldg(p.bm.aabb + a);
                 aU[a] = __ldg(p.bm.aabb + 3 + a);
             }
-#if ARTEMIS_RCP_CROSSING
+            if constexpr (kFast) {
 #pragma unroll
-            for (int a = 0; a < 3; ++a) rg[a] = recip_for_crossings(og[a], dg[a]);
-#endif
+                for (int a = 0; a < 3; ++a) rg[a] = dg[a] != 0.0 ? __drcp_rn(dg[a]) : 0.0;
+            }
             double t0 = p.t_min, t1 = p.t_max;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
@@ -681,8 +680,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 if (dg[a] == 0.0) {
                     if (og[a] < lo || og[a] >= hi) return;
                 } else {  // the slab test's exact plane distances (_core.pyx:252-285)
-                    double ta = crossing(aL[a], og[a], dg[a], rg[a]);
-                    double tb = crossing(aU[a], og[a], dg[a], rg[a]);
+                    double ta = crossing<kFast>(aL[a], og[a], dg[a], rg[a]);
+                    double tb = crossing<kFast>(aU[a], og[a], dg[a], rg[a]);
                     if (ta > tb) {
                         const double sw = ta;
                         ta = tb;
@@ -704,7 +703,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 } else {
                     cs[a] = dg[a] > 0.0 ? 1 : -1;
                     double E;
-                    sync_axis(og[a], dg[a], rg[a], t0, aL[a], aU[a] - 1, cc[a], E, cX[a]);
+                    sync_axis<kFast>(og[a], dg[a], rg[a], t0, aL[a], aU[a] - 1, cc[a], E, cX[a]);
                     t_in = fmax(t_in, E);
                 }
                 cb[a] = cc[a] >> 3;
@@ -1094,7 +1093,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 // grid so a test can vary the ray-to-warp schedule; results must not change
 static int g_render_block_cap = 0;
 
-template <int kMode, int kRays, bool kVec, bool kDDA>
+template <int kMode, int kRays, bool kVec, bool kDDA, bool kFast = false>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
     if (warps == 0) return ARTEMIS_OK;
     const int cp = kVec ? a.channels : (a.channels | 1);
@@ -1106,7 +1105,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
     case D: {                                                                                   \
-        auto kern = render_kernel<D, kMode, kRays, kVec, kDDA>;                                 \
+        auto kern = render_kernel<D, kMode, kRays, kVec, kDDA, kFast>;                          \
         if (smem > 48 * 1024)                                                                   \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         int occ = 0;                                                                            \
@@ -1130,6 +1129,9 @@ int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream
                      (reinterpret_cast<uintptr_t>(a.coef) & 15) == 0;
     const bool dda = a.bm.table != nullptr;
     if (kRays != 0) {  // the device pipeline always has a brick map
+        if (a.fast_div && ARTEMIS_RCP_CROSSING)  // cameras in div_fast's operand ranges
+            return vec ? launch_render_vec<kMode, kRays, true, true, true>(degree, a, warps, st)
+                       : launch_render_vec<kMode, kRays, false, true, true>(degree, a, warps, st);
         return vec ? launch_render_vec<kMode, kRays, true, true>(degree, a, warps, st)
                    : launch_render_vec<kMode, kRays, false, true>(degree, a, warps, st);
     }
@@ -1211,8 +1213,9 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
                   float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
-                  int outputs_ready, cudaStream_t st) {
+                  int outputs_ready, int fast_div, cudaStream_t st) {
     RenderArgs a{};
+    a.fast_div = fast_div;
     {   // a FLUT that fits in half the L2 stays resident: prefetching its rows only costs
         static int l2 = 0;
         if (!l2) {
@@ -1471,9 +1474,11 @@ __global__ void division_selftest_kernel(int64_t n, uint64_t seed,
                 d = rand_normal_bits(st, -400, 400);
         }
         if (d == 0.0 || !isfinite(num) || !isfinite(d)) continue;
-        const double an = fabs(num);  // div_exact's contract: the caller vouches for the dividend
-        const double r = (num == 0.0 || (an >= 0x1p-400 && an <= 0x1p400)) ? recip_for_div(d) : 0.0;
-        const double fast = div_exact(num, d, r);
+        // div_fast where its operand-range contract holds (dividend 0 or in
+        // [2^-400, 2^400], divisor in [2^-600, 2^600]), as the launches use it
+        const bool in_range = div_operand_ok(num, 0x1p-400, 0x1p400) &&
+                              div_operand_ok(d, 0x1p-600, 0x1p600);
+        const double fast = in_range ? div_fast(num, d, __drcp_rn(d)) : __ddiv_rn(num, d);
         const double ref = __ddiv_rn(num, d);
         if (__double_as_longlong(fast) != __double_as_longlong(ref) && !(isnan(fast) && isnan(ref))) {
             ++bad;

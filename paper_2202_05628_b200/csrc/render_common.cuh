@@ -50,6 +50,7 @@ struct RenderArgs {
     float coord_max;  // upper bound of every box coordinate (grid resolution)
     double sigma_dep;
     int early_stop;
+    int fast_div;  // camera launch whose operand ranges allow div_fast (camera_fast_div_ok)
     int no_row_prefetch;  // skip the L2 prefetch of queued rows (FLUT already L2-resident)
     // outputs
     float *F;
@@ -130,56 +131,37 @@ struct CamRecip {
 
 __device__ __forceinline__ CamRecip camera_recip(const artemis_camera &c) {
     CamRecip k;
-    k.rfx = recip_for_div(c.fx);
-    k.rfy = recip_for_div(c.fy);
+    k.rfx = __drcp_rn(c.fx);
+    k.rfy = __drcp_rn(c.fy);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        k.rcell[a] = recip_for_div(c.cell[a]);
+        k.rcell[a] = __drcp_rn(c.cell[a]);
         k.og[a] = __ddiv_rn(__dadd_rn(c.origin[a], -c.lo[a]), c.cell[a]);
     }
     return k;
 }
 
 // camera_ray with every division by a per-view constant (and the per-ray
-// norm) done as a reciprocal-corrected division: the same bits, shorter
-// dependent chains at ray start. Dividends: (u + 0.5) - cx is 0 or >= 2^-53
-// |cx| in magnitude for any sane principal point, d[a] and dw[a] are 0 or
-// >= ~1e-17 for rotations away from underflow; a ray with an operand outside
-// div_exact's range falls back to camera_ray (checked here, never taken on
-// real cameras).
-__device__ __forceinline__ bool div_ok(double n) {
-    const double an = fabs(n);
-    return n == 0.0 || (an >= 0x1p-400 && an <= 0x1p400);
-}
-
+// norm) done by div_fast: the same bits, shorter dependent chains at ray
+// start. Only for launches whose cameras passed camera_fast_div_ok (frame.cu):
+// then (u + 0.5) - cx is 0 or >= 2^-353, |d[a]| is 0 or >= 2^-427 and the
+// norm is >= 1, so every quotient stays far inside the normal range.
 __device__ __forceinline__ void camera_ray_fast(const artemis_camera &c, const CamRecip &k,
                                                 int u, int v, double og[3], double dg[3],
                                                 double dw[3]) {
-    const double n0 = __dadd_rn(__dadd_rn((double)u, 0.5), -c.cx);
-    const double n1 = __dadd_rn(__dadd_rn((double)v, 0.5), -c.cy);
-    if (k.rfx == 0.0 || k.rfy == 0.0 || !div_ok(n0) || !div_ok(n1)) {
-        camera_ray(c, u, v, og, dg, dw);
-        return;
-    }
-    const double c0 = div_exact(n0, c.fx, k.rfx);
-    const double c1 = div_exact(n1, c.fy, k.rfy);
+    const double c0 = div_fast(__dadd_rn(__dadd_rn((double)u, 0.5), -c.cx), c.fx, k.rfx);
+    const double c1 = div_fast(__dadd_rn(__dadd_rn((double)v, 0.5), -c.cy), c.fy, k.rfy);
     double d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
         d[a] = __fma_rn(1.0, c.R[3 * a + 2], __fma_rn(c1, c.R[3 * a + 1], __dmul_rn(c0, c.R[3 * a])));
     const double nrm = __dsqrt_rn(
         __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
-    const double rn = recip_for_div(nrm);
-    if (rn == 0.0 || !div_ok(d[0]) || !div_ok(d[1]) || !div_ok(d[2])) {
-        camera_ray(c, u, v, og, dg, dw);
-        return;
-    }
+    const double rn = __drcp_rn(nrm);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        dw[a] = div_exact(d[a], nrm, rn);
-        // |dw| <= 1 and 0 or >= |d[a]| / nrm: in range; the cell reciprocal
-        // is 0 (-> __ddiv_rn) for an out-of-range cell size
-        dg[a] = div_ok(dw[a]) ? div_exact(dw[a], c.cell[a], k.rcell[a]) : __ddiv_rn(dw[a], c.cell[a]);
+        dw[a] = div_fast(d[a], nrm, rn);
+        dg[a] = div_fast(dw[a], c.cell[a], k.rcell[a]);
         og[a] = k.og[a];
     }
 }

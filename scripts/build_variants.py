@@ -14,6 +14,8 @@ VARIANTS = {
     "rcp": ("ARTEMIS_RCP_CROSSING=1",),
     "norcp": ("ARTEMIS_RCP_CROSSING=0", "ARTEMIS_FAST_CAMRAY=0"),
     "slowcam": ("ARTEMIS_FAST_CAMRAY=0",),
+    "noguard": ("ARTEMIS_GUARD_DIV=0",),
+    "noguard_slowcam": ("ARTEMIS_GUARD_DIV=0", "ARTEMIS_FAST_CAMRAY=0"),
     "q4b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48", "ARTEMIS_MIN_BLOCKS=5"),
     "q4t40b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=40", "ARTEMIS_MIN_BLOCKS=5"),
     "q4t56b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=56", "ARTEMIS_MIN_BLOCKS=5"),

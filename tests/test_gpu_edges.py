@@ -231,3 +231,40 @@ def test_counting_rebuild_equals_sort_path(monkeypatch, nan_rows):
                                    flut64=sc.flut32[:, -1:].astype(np.float64))
         assert np.array_equal(t1["codes"], want["tree"][0])
         assert np.array_equal(t1["flut_idx"], want["tree"][1])
+
+
+def test_fast_division_path_equals_ddiv(monkeypatch):
+    """Camera frames whose operands are in div_fast's range compute every
+    plane crossing and camera-ray division as a reciprocal-corrected
+    product (bricks.cuh); ARTEMIS_FAST_DIV=0 forces __ddiv_rn. Same maps,
+    bit for bit, for single views, multi-view launches and tile shards; a
+    camera outside the range (subnormal principal point) falls back by itself
+    and still matches the oracle."""
+    from paper_2202_05628_b200.frame import FramePipeline
+
+    sc = S.make_scene("c1", frames=1, image=(120, 88))
+    pose = KM.PoseSpec.make(sc.poses[0])
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ARTEMIS_FAST_DIV", mode)
+        fp = FramePipeline.from_scene(sc)
+        res = [x.clone() for x in fp.run(pose, sc.cameras[0][1], graph=False)]
+        res += [x.clone() for x in fp.run(pose, sc.cameras[0][2], graph=True)]
+        res += [x for v in fp.render_views(pose, sc.cameras[0][:3], graph=False) for x in v]
+        res += [x.clone() for x in fp.run(pose, sc.cameras[0][5], graph=False, tiles=(0, 2))]
+        fp.stream.synchronize()
+        out[mode] = res
+        fp.close()
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
+    monkeypatch.delenv("ARTEMIS_FAST_DIV")
+    cam = dataclasses.replace(sc.cameras[0][0], cx=5e-324)
+    fp = FramePipeline.from_scene(sc)
+    F, A, D = fp.run(pose, cam, graph=False)
+    fp.stream.synchronize()
+    tables = KM.pose_tables(sc.rig, pose)
+    want = oracle.render_frame(sc, tables, cam)
+    err = np.abs(F.cpu().numpy().astype(np.float64) - want["F"])
+    assert err.max() <= 1e-4 and err.mean() <= 1e-5
+    assert np.array_equal(D.cpu().numpy(), want["D"].astype(np.float32))
+    fp.close()
