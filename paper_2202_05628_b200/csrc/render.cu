@@ -77,6 +77,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_STREAM_OUT
 #define ARTEMIS_STREAM_OUT 0  // 1: output maps stored evict-first (st.global.cs)
 #endif
+#ifndef ARTEMIS_A_CHECK
+#define ARTEMIS_A_CHECK 1  // phase A: steps between checks of the warp's queued total
+#endif
 #ifndef ARTEMIS_FAST_CAMRAY
 #define ARTEMIS_FAST_CAMRAY 1  // camera rays with reciprocal-corrected divisions
 #endif
@@ -746,6 +749,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const bool can = walking && nq < kQCap;
             if (__ballot_sync(0xffffffffu, can) == 0) break;
             if (can) step();
+#if ARTEMIS_A_CHECK > 1
+            // the warp's queued total is checked every ARTEMIS_A_CHECK steps
+            // (a warp reduction per step sits on the walk's critical path)
+            if ((it % ARTEMIS_A_CHECK) != ARTEMIS_A_CHECK - 1) continue;
+#endif
             if (__reduce_add_sync(0xffffffffu, (unsigned)nq) >= (unsigned)kQThresh) break;
         }
         ARTEMIS_PHASE(2);

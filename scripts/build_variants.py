@@ -14,8 +14,12 @@ VARIANTS = {
     "rcp": ("ARTEMIS_RCP_CROSSING=1",),
     "norcp": ("ARTEMIS_RCP_CROSSING=0", "ARTEMIS_FAST_CAMRAY=0"),
     "slowcam": ("ARTEMIS_FAST_CAMRAY=0",),
-    "noguard": ("ARTEMIS_GUARD_DIV=0",),
-    "noguard_slowcam": ("ARTEMIS_GUARD_DIV=0", "ARTEMIS_FAST_CAMRAY=0"),
+    "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
+    "ac2": ("ARTEMIS_A_CHECK=2",),
+    "ac3": ("ARTEMIS_A_CHECK=3",),
+    "ac2t40": ("ARTEMIS_A_CHECK=2", "ARTEMIS_QTHRESH=40"),
+    "t40": ("ARTEMIS_QTHRESH=40",),
+    "t56": ("ARTEMIS_QTHRESH=56",),
     "q4b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48", "ARTEMIS_MIN_BLOCKS=5"),
     "q4t40b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=40", "ARTEMIS_MIN_BLOCKS=5"),
     "q4t56b5": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=56", "ARTEMIS_MIN_BLOCKS=5"),
@@ -29,7 +33,6 @@ VARIANTS = {
     "q4t48": ("ARTEMIS_QCAP=4", "ARTEMIS_QTHRESH=48"),
     "b3": ("ARTEMIS_MIN_BLOCKS=3",),
     "b5": ("ARTEMIS_MIN_BLOCKS=5",),
-    "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
     "noshade": ("ARTEMIS_NOSHADE=1",),
     "q5t56": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=56"),
     "q5t64": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=64"),
