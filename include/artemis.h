@@ -166,6 +166,12 @@ typedef struct {
     const double *dirs_w;       /* (R, 3) unit world directions (SH input) */
     int64_t n_rays;
     double t_min, t_max;
+    int32_t fast_div;           /* 1: the caller vouches that every origins_g
+                                   component is 0 or of magnitude in [2^-300, 2^300]
+                                   and every dirs_g component 0 or in
+                                   [2^-600, 2^300]; the cell walk then divides by
+                                   a corrected reciprocal (same bits, faster).
+                                   0: __ddiv_rn. */
 } artemis_rays;
 
 /* Pinhole camera, evaluated per pixel exactly as rays_for_camera

@@ -45,7 +45,7 @@ class Shading(C.Structure):
 
 class Rays(C.Structure):
     _fields_ = [("origins_g", P), ("dirs_g", P), ("dirs_w", P), ("n_rays", I64),
-                ("t_min", DBL), ("t_max", DBL)]
+                ("t_min", DBL), ("t_max", DBL), ("fast_div", I32)]
 
 
 class Camera(C.Structure):

@@ -1143,9 +1143,13 @@ int launch_render_deg(int degree, const RenderArgs &a, int64_t warps, cudaStream
         return vec ? launch_render_vec<kMode, kRays, true, true>(degree, a, warps, st)
                    : launch_render_vec<kMode, kRays, false, true>(degree, a, warps, st);
     }
-    if (dda)
+    if (dda) {
+        if (a.fast_div && ARTEMIS_RCP_CROSSING)  // rays vouched for by the caller
+            return vec ? launch_render_vec<kMode, kRays, true, true, true>(degree, a, warps, st)
+                       : launch_render_vec<kMode, kRays, false, true, true>(degree, a, warps, st);
         return vec ? launch_render_vec<kMode, kRays, true, true>(degree, a, warps, st)
                    : launch_render_vec<kMode, kRays, false, true>(degree, a, warps, st);
+    }
     return vec ? launch_render_vec<kMode, kRays, true, false>(degree, a, warps, st)
                : launch_render_vec<kMode, kRays, false, false>(degree, a, warps, st);
 }
@@ -1183,6 +1187,7 @@ static void fill_rays(RenderArgs &a, const artemis_rays *r) {
     a.n_rays = r->n_rays;
     a.t_min = r->t_min;
     a.t_max = r->t_max;
+    a.fast_div = r->fast_div;
 }
 
 template <typename T>

@@ -385,22 +385,43 @@ def _trace_shading(rows: int):
     return shading_for(np.zeros((rows, 2)), np.zeros(rows, np.int32), np.eye(3)[None], 0, 1)
 
 
+def _in_range_or_zero(a, lo: float, hi: float) -> bool:
+    """Every element 0 or of magnitude in [lo, hi] (numpy or torch)."""
+    if isinstance(a, torch.Tensor):
+        m = a.abs()
+        return bool(((a == 0) | ((m >= lo) & (m <= hi))).all().item())
+    m = np.abs(a)
+    return bool(np.all((a == 0) | ((m >= lo) & (m <= hi))))
+
+
+def fast_div_ok(og, dg) -> bool:
+    """The operand ranges under which the cell walk's reciprocal-corrected
+    division is exact for every crossing (artemis_rays.fast_div, bricks.cuh):
+    grid-space origins 0 or in [2^-300, 2^300], directions 0 or in
+    [2^-600, 2^300]. Real rays always qualify; anything else takes __ddiv_rn."""
+    return _in_range_or_zero(og, 2.0 ** -300, 2.0 ** 300) and \
+        _in_range_or_zero(dg, 2.0 ** -600, 2.0 ** 300)
+
+
 class DeviceRays:
     def __init__(self, origins_g, dirs_g, dirs_w, t_min, t_max):
-        self.og = upload(np.asarray(origins_g).reshape(-1, 3), np.float64)
-        self.dg = upload(np.asarray(dirs_g).reshape(-1, 3), np.float64)
+        og = np.asarray(origins_g, dtype=np.float64).reshape(-1, 3)
+        dg = np.asarray(dirs_g, dtype=np.float64).reshape(-1, 3)
+        self.og = upload(og, np.float64)
+        self.dg = upload(dg, np.float64)
         self.dw = upload(np.asarray(dirs_w).reshape(-1, 3), np.float64) if dirs_w is not None \
             else self.dg
         self.n = self.og.shape[0]
         self.view = _lib.Rays(ptr(self.og), ptr(self.dg), ptr(self.dw), self.n, float(t_min),
-                              float(t_max))
+                              float(t_max), int(fast_div_ok(og, dg)))
 
     @staticmethod
     def from_tensors(og, dg, dw, t_min=0.0, t_max=np.inf):
         r = DeviceRays.__new__(DeviceRays)
         r.og, r.dg, r.dw = og, dg, dw
         r.n = og.shape[0]
-        r.view = _lib.Rays(ptr(og), ptr(dg), ptr(dw), r.n, float(t_min), float(t_max))
+        r.view = _lib.Rays(ptr(og), ptr(dg), ptr(dw), r.n, float(t_min), float(t_max),
+                           int(fast_div_ok(og, dg)) if r.n else 0)
         return r
 
 

@@ -268,3 +268,24 @@ def test_fast_division_path_equals_ddiv(monkeypatch):
     assert err.max() <= 1e-4 and err.mean() <= 1e-5
     assert np.array_equal(D.cpu().numpy(), want["D"].astype(np.float32))
     fp.close()
+
+
+def test_api_fast_division_equals_ddiv(monkeypatch):
+    """The flat-array API path (render_rays / forward_fit on the brick walk)
+    takes the reciprocal-corrected division when the rays' operand ranges
+    qualify (kernels.fast_div_ok); forcing __ddiv_rn gives the same bits."""
+    from paper_2202_05628_b200 import kernels as K
+
+    sc = S.make_scene("c0", frames=1, image=(96, 96))
+    tables = KM.pose_tables(sc.rig, KM.PoseSpec.make(sc.poses[0]))
+    fr = oracle.render_frame(sc, tables, sc.cameras[0][0], render=False)
+    args = (*fr["tree"], fr["origins_g"], fr["dirs_g"], fr["dirs_w"], 0.0, np.inf, sc.flut32,
+            fr["rotation_joint"], tables.rot_inv, sc.degree, sc.channels)
+    assert K.fast_div_ok(fr["origins_g"], fr["dirs_g"])
+    fast = (*K.render_rays(*args, sc.lambda_th, sc.sigma_dep, True), *K.forward_fit(*args))
+    monkeypatch.setattr(K, "fast_div_ok", lambda og, dg: False)
+    slow = (*K.render_rays(*args, sc.lambda_th, sc.sigma_dep, True), *K.forward_fit(*args))
+    for a, b in zip(fast, slow):
+        assert np.array_equal(a, b)
+    assert not K.fast_div_ok(np.array([[1e-320, 1.0, 2.0]]), np.ones((1, 3)))
+    assert not K.fast_div_ok(np.ones((1, 3)), np.array([[1e-200, 0.0, 1.0]]))
