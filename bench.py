@@ -650,15 +650,11 @@ def measure_e2e(args, sc, fp, run, world, rank, rays_step, red_dev="cuda"):
     else:
         # tiles / views / stereo: host FK every step, the step (+ gather), then
         # every view's F/alpha/depth into persistent dense pinned host maps on
-        # rank 0: per view the covered-pixel bounding box (artemis_frame_bbox)
+        # rank 0 (frame.ViewsReadout: per view the covered-pixel bounding box
         # united with the box that host buffer last received, as 2-D copies
-        # on a copy stream (outside the union both frames are (0, 0, +inf):
+        # on a copy stream -- outside the union both frames are (0, 0, +inf):
         # bit-identical dense maps). Pipelined: step k+1 renders while step
         # k's boxes cross PCIe (two device output sets, two host sets).
-        from paper_2202_05628_b200 import _lib
-        from paper_2202_05628_b200.device import ptr
-
-        L = _lib.lib()
         cs = torch.cuda.Stream()
         Cc = sc.channels
         n = run.W * run.H
@@ -670,8 +666,11 @@ def measure_e2e(args, sc, fp, run, world, rank, rays_step, red_dev="cuda"):
         elif run.tiles and not run.peer:
             outs = [[fp.outputs(run.W, run.H)],
                     [tuple(x.clone() for x in fp.outputs(run.W, run.H))]]
-        sets = [dict(host=None, prev=None, ev_box=None, copied=None, triples=None,
-                     dbox=None, hbox=None) for _ in range(2)]
+        from paper_2202_05628_b200.frame import ViewsReadout
+
+        readers = [None, None]
+        # outputs shared by both sets: the root's peer maps, the gathered views
+        shared_out = run.peer or (args.config == "c1" and world > 1)
 
         def triples_of(res):
             """Flat step results -> [(F (n, C), alpha (n), depth (n))] per view."""
@@ -688,60 +687,20 @@ def measure_e2e(args, sc, fp, run, world, rank, rays_step, red_dev="cuda"):
             return [tuple(res[3 * i:3 * i + 3]) for i in range(len(res) // 3)]
 
         def enqueue(s, b):
-            st = sets[b]
+            for rd in (readers if shared_out else [readers[b]]):
+                if rd is not None and rd.copied is not None:
+                    fp.stream.wait_event(rd.copied)  # its previous D2H has read them
             f = run.frames[args.warmup + s]
             run.tables[f] = KM.pose_tables(sc.rig, KM.PoseSpec.make(sc.poses[f]))
-            for other in (sets if run.peer else [st]):  # peer: one set of maps (the root's)
-                if other["copied"] is not None:
-                    fp.stream.wait_event(other["copied"])  # its previous D2H has read it
             tri = triples_of(run.step(args.warmup + s, outs=outs[b]))
-            st["triples"] = tri
             if not tri:
                 return
-            if st["dbox"] is None:
-                with torch.cuda.stream(fp.stream):
-                    st["dbox"] = torch.empty((len(tri), 4), dtype=torch.int32, device="cuda")
-                st["hbox"] = torch.empty((len(tri), 4), dtype=torch.int32, pin_memory=True)
-                st["host"] = [(torch.zeros((n, Cc), dtype=torch.float32, pin_memory=True),
-                               torch.zeros(n, dtype=torch.float32, pin_memory=True),
-                               torch.full((n,), float("inf"), dtype=torch.float32,
-                                          pin_memory=True)) for _ in tri]
-                st["prev"] = [(run.W, run.H, -1, -1) for _ in tri]  # empty box
-            for i, (F, A, D) in enumerate(tri):
-                check = L.artemis_frame_bbox(ptr(A), ptr(D), 0, run.W, run.H,
-                                             ptr(st["dbox"][i]), fp.stream.cuda_stream or None)
-                assert check == 0
-            with torch.cuda.stream(fp.stream):
-                st["hbox"].copy_(st["dbox"], non_blocking=True)
-            st["ev_box"] = torch.cuda.Event()
-            st["ev_box"].record(fp.stream)
+            if readers[b] is None:
+                readers[b] = ViewsReadout(tri, run.W, run.H, Cc)
+            readers[b].mark(fp.stream)
 
         def finish(b):
-            """Boxes of set b are on the host once its render is done: issue the
-            union-box 2-D copies of every view on the copy stream."""
-            st = sets[b]
-            if not st["triples"]:
-                return 0
-            st["ev_box"].synchronize()
-            cs.wait_event(st["ev_box"])
-            nbytes = 0
-            for i, (F, A, D) in enumerate(st["triples"]):
-                x0, y0, x1, y1 = (int(v) for v in st["hbox"][i])
-                px0, py0, px1, py1 = st["prev"][i]
-                ux0, uy0, ux1, uy1 = min(x0, px0), min(y0, py0), max(x1, px1), max(y1, py1)
-                st["prev"][i] = (x0 if x1 >= 0 else run.W, y0 if y1 >= 0 else run.H, x1, y1)
-                if ux1 < 0 or uy1 < 0:
-                    continue
-                hF, hA, hD = st["host"][i]
-                rows = uy1 - uy0 + 1
-                for dev, hst, per in ((F, hF, 4 * Cc), (A, hA, 4), (D, hD, 4)):
-                    assert L.artemis_copy_rect_d2h(hst.data_ptr(), ptr(dev), run.W * per,
-                                                   ux0 * per, (ux1 - ux0 + 1) * per, uy0, rows,
-                                                   cs.cuda_stream or None) == 0
-                    nbytes += (ux1 - ux0 + 1) * per * rows
-            st["copied"] = torch.cuda.Event()
-            st["copied"].record(cs)
-            return nbytes
+            return readers[b].copy(cs) if readers[b] is not None else 0
 
         for w_ in range(2):  # warm both sets (graphs, pinned buffers)
             enqueue(w_, w_)

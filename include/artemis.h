@@ -493,6 +493,18 @@ int artemis_frame_bbox(const void *alpha, const void *depth, int maps64, int wid
                        int32_t *box, artemis_stream stream);
 int artemis_copy_rect_d2h(void *dst_host, const void *src_dev, size_t row_pitch, size_t x_bytes,
                           size_t width_bytes, int64_t y0, int64_t rows, artemis_stream stream);
+/* The same for several views of one size (multi-view / stereo frames):
+ * artemis_views_bbox writes every view's box (device n_views x 4; alpha and
+ * depth are HOST arrays of n_views device pointers); artemis_views_copy_union_d2h
+ * refreshes n_views dense host frames from those boxes (host n_views x 4)
+ * united with each host buffer's previous box (prev, host, updated), dev/host
+ * being n_views x 3 pointer arrays {F, alpha, depth}; *bytes = bytes moved. */
+int artemis_views_bbox(const void *const *alpha, const void *const *depth, int n_views,
+                       int maps64, int width, int height, int32_t *boxes, artemis_stream stream);
+int artemis_views_copy_union_d2h(int n_views, const int32_t *boxes, int32_t *prev,
+                                 const void *const *dev, void *const *host, int width,
+                                 int height, int channels, int maps64, int64_t *bytes,
+                                 artemis_stream stream);
 
 /* ---- Multi-GPU tile shards ----------------------
  * With tile sharding (artemis_camera tile_start/tile_stride) each rank packs

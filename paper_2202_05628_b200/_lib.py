@@ -130,6 +130,8 @@ _SIGS = {
     "artemis_host_expand": (INT, [P, I64, INT, P, I64, P, P, P, P, INT]),
     "artemis_frame_bbox": (INT, [P, P, INT, INT, INT, P, P]),
     "artemis_copy_rect_d2h": (INT, [P, P, SZ, SZ, SZ, I64, I64, P]),
+    "artemis_views_bbox": (INT, [P, P, INT, INT, INT, INT, P, P]),
+    "artemis_views_copy_union_d2h": (INT, [INT, P, P, P, P, INT, INT, INT, INT, P, P]),
     "artemis_l1_grads": (INT, [P, P, P, P, I64, INT, P, P, P, P, P]),
     "artemis_mark_touched": (INT, [P, I64, P, P]),
     "artemis_vrt_workspace_bytes": (SZ, [I64, I64]),

@@ -256,3 +256,55 @@ extern "C" int artemis_copy_rect_d2h(void *dst_host, const void *src_dev, size_t
                                   width_bytes, (size_t)rows, cudaMemcpyDeviceToHost, S(stream)));
     return ARTEMIS_OK;
 }
+
+// Several views' covered-pixel boxes in one call (boxes: device, n_views x 4).
+extern "C" int artemis_views_bbox(const void *const *alpha, const void *const *depth,
+                                  int n_views, int maps64, int width, int height, int32_t *boxes,
+                                  artemis_stream stream) {
+    if (!alpha || !depth || !boxes || n_views < 1) return ARTEMIS_ERR_ARG;
+    for (int v = 0; v < n_views; ++v) {
+        const int rc = artemis_frame_bbox(alpha[v], depth[v], maps64, width, height, boxes + 4 * v,
+                                          stream);
+        if (rc) return rc;
+    }
+    return ARTEMIS_OK;
+}
+
+// Refresh n_views dense host frames (F fp32 (w*h, C), alpha/depth 4- or
+// 8-byte maps) from their device frames: per view, the union of this frame's
+// box (boxes, host) and the box that host buffer last received (prev, host,
+// updated) as three 2-D copies on `stream`. Outside the union both frames are
+// (0, 0, +inf), so the dense host maps equal the device maps bit for bit.
+// *bytes receives the bytes moved.
+extern "C" int artemis_views_copy_union_d2h(int n_views, const int32_t *boxes, int32_t *prev,
+                                            const void *const *dev, void *const *host,
+                                            int width, int height, int channels, int maps64,
+                                            int64_t *bytes, artemis_stream stream) {
+    if (n_views < 1 || !boxes || !prev || !dev || !host || width < 1 || height < 1 ||
+        channels < 1)
+        return ARTEMIS_ERR_ARG;
+    int64_t moved = 0;
+    const size_t per[3] = {(size_t)channels * 4, maps64 ? 8u : 4u, maps64 ? 8u : 4u};
+    for (int v = 0; v < n_views; ++v) {
+        const int32_t *b = boxes + 4 * v;
+        int32_t *p = prev + 4 * v;
+        const int ux0 = std::min(b[0], p[0]), uy0 = std::min(b[1], p[1]);
+        const int ux1 = std::max(b[2], p[2]), uy1 = std::max(b[3], p[3]);
+        // remember this frame's box (empty -> an empty box that unions to nothing)
+        p[0] = b[2] >= 0 ? b[0] : width;
+        p[1] = b[3] >= 0 ? b[1] : height;
+        p[2] = b[2];
+        p[3] = b[3];
+        if (ux1 < 0 || uy1 < 0 || ux0 > ux1 || uy0 > uy1) continue;
+        const int64_t rows = uy1 - uy0 + 1;
+        for (int m = 0; m < 3; ++m) {
+            const int rc = artemis_copy_rect_d2h(host[3 * v + m], dev[3 * v + m], width * per[m],
+                                                 ux0 * per[m], (ux1 - ux0 + 1) * per[m], uy0, rows,
+                                                 stream);
+            if (rc) return rc;
+            moved += (int64_t)(ux1 - ux0 + 1) * per[m] * rows;
+        }
+    }
+    if (bytes) *bytes = moved;
+    return ARTEMIS_OK;
+}

@@ -576,3 +576,62 @@ class FramePipeline:
             self.close()
         except Exception:
             pass
+
+
+class ViewsReadout:
+    """Dense pinned host copies of a fixed set of device frames (views of
+    one size: multi-view / stereo / gathered tiles), refreshed per frame by
+    the covered-pixel box of each view united with the box its host buffer
+    last received (artemis_views_bbox + artemis_views_copy_union_d2h: two
+    native calls per frame however many views). `mark(stream)` enqueues the
+    boxes after the frame; `copy(copy_stream)` waits for them and issues the
+    2-D copies; the host maps are valid once `copied` has completed."""
+
+    def __init__(self, triples, width: int, height: int, channels: int, maps64: bool = False):
+        L = _lib.lib()
+        self.L = L
+        self.n = len(triples)
+        self.w, self.h, self.c = int(width), int(height), int(channels)
+        self.maps64 = bool(maps64)
+        mt = torch.float64 if maps64 else torch.float32
+        n = self.w * self.h
+        self.triples = list(triples)
+        self.host = [(torch.zeros((n, self.c), dtype=torch.float32, pin_memory=True),
+                      torch.zeros(n, dtype=mt, pin_memory=True),
+                      torch.full((n,), float("inf"), dtype=mt, pin_memory=True))
+                     for _ in range(self.n)]
+        self.dbox = torch.empty((self.n, 4), dtype=torch.int32, device="cuda")
+        self.hbox = torch.empty((self.n, 4), dtype=torch.int32, pin_memory=True)
+        self.prev = np.tile(np.array([self.w, self.h, -1, -1], dtype=np.int32), (self.n, 1))
+        pa = C.c_void_p * self.n
+        self._A = pa(*[ptr(t[1]) for t in self.triples])
+        self._D = pa(*[ptr(t[2]) for t in self.triples])
+        p3 = C.c_void_p * (3 * self.n)
+        self._dev = p3(*[ptr(x) for t in self.triples for x in t])
+        self._host = p3(*[x.data_ptr() for t in self.host for x in t])
+        self.boxed = None
+        self.copied = None
+        self.last_bytes = 0
+
+    def mark(self, stream: torch.cuda.Stream) -> None:
+        st = stream.cuda_stream or None
+        check(self.L.artemis_views_bbox(C.cast(self._A, C.c_void_p), C.cast(self._D, C.c_void_p),
+                                        self.n, int(self.maps64), self.w, self.h,
+                                        ptr(self.dbox), st), "views_bbox")
+        with torch.cuda.stream(stream):
+            self.hbox.copy_(self.dbox, non_blocking=True)
+        self.boxed = torch.cuda.Event()
+        self.boxed.record(stream)
+
+    def copy(self, copy_stream: torch.cuda.Stream) -> int:
+        self.boxed.synchronize()
+        copy_stream.wait_event(self.boxed)
+        moved = C.c_int64(0)
+        check(self.L.artemis_views_copy_union_d2h(
+            self.n, self.hbox.data_ptr(), self.prev.ctypes.data, C.cast(self._dev, C.c_void_p),
+            C.cast(self._host, C.c_void_p), self.w, self.h, self.c, int(self.maps64),
+            C.byref(moved), copy_stream.cuda_stream or None), "views_copy")
+        self.copied = torch.cuda.Event()
+        self.copied.record(copy_stream)
+        self.last_bytes = int(moved.value)
+        return self.last_bytes
