@@ -691,7 +691,7 @@ def measure_e2e(args, sc, fp, run, world, rank, rays_step, red_dev="cuda"):
                 if rd is not None and rd.copied is not None:
                     fp.stream.wait_event(rd.copied)  # its previous D2H has read them
             f = run.frames[args.warmup + s]
-            run.tables[f] = KM.pose_tables(sc.rig, KM.PoseSpec.make(sc.poses[f]))
+            run.tables[f] = fp.tables(KM.PoseSpec.make(sc.poses[f]))  # host FK (canonical cached)
             tri = triples_of(run.step(args.warmup + s, outs=outs[b]))
             if not tri:
                 return

@@ -50,7 +50,7 @@ namespace artemis {
 #define ARTEMIS_DEDUP 1
 #endif
 #ifndef ARTEMIS_ROW_PREFETCH
-#define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line
+#define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line, 3 into L1
 #endif
 namespace {
 constexpr int kRenderWarps = 4;
@@ -794,8 +794,13 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #if ARTEMIS_ROW_PREFETCH
                 if (!p.no_row_prefetch) {  // the row's 9 x 128 B lines are read in phase C
                     const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
-                    for (int off = 0; off < (ARTEMIS_ROW_PREFETCH == 2 ? 1 : p.coef_stride * 4); off += 128)
+                    for (int off = 0; off < (ARTEMIS_ROW_PREFETCH == 2 ? 1 : p.coef_stride * 4); off += 128) {
+#if ARTEMIS_ROW_PREFETCH == 3
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(row + off));
+#else
                         prefetch_l2(row + off);
+#endif
+                    }
                 }
 #endif
                 const double sigma = __longlong_as_double(((long long)L2.y << 32) | L2.x);

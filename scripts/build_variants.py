@@ -15,6 +15,7 @@ VARIANTS = {
     "norcp": ("ARTEMIS_RCP_CROSSING=0", "ARTEMIS_FAST_CAMRAY=0"),
     "slowcam": ("ARTEMIS_FAST_CAMRAY=0",),
     "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
+    "pfl1": ("ARTEMIS_ROW_PREFETCH=3",),
     "ac2": ("ARTEMIS_A_CHECK=2",),
     "ac3": ("ARTEMIS_A_CHECK=3",),
     "ac2t40": ("ARTEMIS_A_CHECK=2", "ARTEMIS_QTHRESH=40"),
