@@ -77,6 +77,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_STREAM_OUT
 #define ARTEMIS_STREAM_OUT 0  // 1: output maps stored evict-first (st.global.cs)
 #endif
+#ifndef ARTEMIS_SMEM_MASK
+#define ARTEMIS_SMEM_MASK 0  // 1: the walk's brick mask cached in shared memory per lane
+#endif
 #ifndef ARTEMIS_A_CHECK
 #define ARTEMIS_A_CHECK 1  // phase A: steps between checks of the warp's queued total
 #endif
@@ -405,6 +408,24 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
     // transmittance chain (T, accumulated alpha, depth): touched once per
     // round (phase B2) and at retirement, so it lives in shared memory
     double *s_tad = s_dw + 3 * kRenderThreads + 3 * tid;
+    // the current brick's 512-bit occupancy mask per lane (cell walk), word-
+    // major so a warp's lanes read distinct banks: one L2 round trip per
+    // brick entered instead of one per cell step
+    uint32_t *s_mask = reinterpret_cast<uint32_t *>(s_dw + 6 * kRenderThreads);
+    auto load_mask = [&]() {
+#if ARTEMIS_SMEM_MASK
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.bm.recs[cbid].mask);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 v = __ldg(src + q4);
+            s_mask[(4 * q4) * kRenderThreads + tid] = v.x;
+            s_mask[(4 * q4 + 1) * kRenderThreads + tid] = v.y;
+            s_mask[(4 * q4 + 2) * kRenderThreads + tid] = v.z;
+            s_mask[(4 * q4 + 3) * kRenderThreads + tid] = v.w;
+        }
+#endif
+    };
+    (void)s_mask;
     int64_t hits = 0, trace_base = 0;
     int rv = 0;  // camera mode: view of this lane's ray
     int cur = kEnd, top = 0, nq = 0;
@@ -485,7 +506,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                     cTb[a] = brick_exit(a);
                 }
             cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
-            if (cbid >= 0) enter_brick(adv, tn);
+            if (cbid >= 0) {
+                load_mask();
+                enter_brick(adv, tn);
+            }
             return;
         }
         ARTEMIS_STAT(1);
@@ -496,7 +520,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
         const uint32_t m = spread3_small(cc[0] & 7) | (spread3_small(cc[1] & 7) << 1) |
                            (spread3_small(cc[2] & 7) << 2);
         const BrickRec &R = p.bm.recs[cbid];
+#if ARTEMIS_SMEM_MASK
+        const uint32_t word = s_mask[(m >> 5) * kRenderThreads + tid];  // cached at brick entry
+#else
         const uint32_t word = __ldg(&R.mask[m >> 5]);
+#endif
         if (((word >> (m & 31u)) & 1u) && t1 > t0) {
             const uint32_t leaf = __ldg(&R.first) + (uint32_t)__ldg(&R.prefix[m >> 5]) +
                                   (uint32_t)__popc(word & ((1u << (m & 31u)) - 1u));
@@ -531,7 +559,10 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 }
             new_brick |= bchg;
         }
-        if (new_brick) cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
+        if (new_brick) {
+            cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
+            if (cbid >= 0) load_mask();
+        }
     };
     auto step = [&]() {
         if constexpr (kDDA) {
@@ -714,6 +745,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #pragma unroll
             for (int a = 0; a < 3; ++a) cTb[a] = brick_exit(a);
             cbid = brick_lookup(p.bm, cb[0], cb[1], cb[2]);
+            if (cbid >= 0) load_mask();
             walking = true;
         }
     };
@@ -1113,7 +1145,8 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
     const size_t feat_bytes = 4;
     const size_t smem = stack_bytes(kDDA) + queue_bytes(kRays == 1 || kRays == 3) +
                         (kMode == kCount ? 0 : (size_t)kRenderWarps * 32 * cp * feat_bytes) +
-                        (size_t)kRenderWarps * 32 * kQCap * (2 + 4) + (size_t)kRenderThreads * 6 * 8;
+                        (size_t)kRenderWarps * 32 * kQCap * (2 + 4) + (size_t)kRenderThreads * 6 * 8 +
+                        (kDDA && ARTEMIS_SMEM_MASK ? (size_t)kRenderThreads * 64 : 0);
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \

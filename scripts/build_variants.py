@@ -16,6 +16,7 @@ VARIANTS = {
     "slowcam": ("ARTEMIS_FAST_CAMRAY=0",),
     "nopf": ("ARTEMIS_ROW_PREFETCH=0",),
     "pfl1": ("ARTEMIS_ROW_PREFETCH=3",),
+    "smask": ("ARTEMIS_SMEM_MASK=1",),
     "ac2": ("ARTEMIS_A_CHECK=2",),
     "ac3": ("ARTEMIS_A_CHECK=3",),
     "ac2t40": ("ARTEMIS_A_CHECK=2", "ARTEMIS_QTHRESH=40"),
