@@ -332,7 +332,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution, &f->bmap};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
-    if (vo.n > 1 && !f->small_flut) {
+    const char *one = getenv("ARTEMIS_VIEWS_ONE_LAUNCH");  // experiment
+    if (vo.n > 1 && !f->small_flut && !(one && one[0] == '1')) {
         // big FLUT: the views' rows would not stay in L2 together (configs[4]
         // stereo: one launch 10.4 ms vs 9.6 ms for two), so one launch per view
         for (int v = 0; v < vo.n && !rc; ++v) {

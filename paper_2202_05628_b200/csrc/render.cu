@@ -23,6 +23,7 @@
 // Packed nodes (tree.cu) give both children's boxes in one 32-byte
 // record, so an internal-node visit is a single sector load.
 #include <math.h>
+#include <stdlib.h>
 #include <math_constants.h>
 
 #include <type_traits>
@@ -631,7 +632,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             if (kMulti) rv = (int)(gi % nv);
             const artemis_camera &cam = p.cam[rv];
             const int64_t t = tstart + (kMulti ? gi / nv : gi) * tstride;
-            const int64_t tile = order ? (int64_t)__ldg(order + t) : t;
+            int64_t tile = order ? (int64_t)__ldg(order + t) : t;
+            if (kMulti && p.view_shift[rv]) {  // experiment: disparity-aligned views
+                const int64_t tx = (tile % p.tiles_x + p.view_shift[rv] + p.tiles_x) % p.tiles_x;
+                tile = (tile / p.tiles_x) * p.tiles_x + tx;
+            }
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
             const int py = (int)(tile / p.tiles_x) * 4 + (sl >> 3);
@@ -1291,6 +1296,14 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
             a.Dv[v] = Dv[v];
         }
         a.n_views = n_views;
+        if (const char *env = getenv("ARTEMIS_VIEW_SHIFT")) {  // experiment: "s0,s1,..."
+            int v = 0;
+            for (const char *c = env; *c && v < n_views; ++v) {
+                a.view_shift[v] = atoi(c);
+                while (*c && *c != ',') ++c;
+                if (*c == ',') ++c;
+            }
+        }
         F = Fv[0];
         A = Av[0];
         D = Dv[0];
