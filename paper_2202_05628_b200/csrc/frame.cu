@@ -51,7 +51,7 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
                   float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
-                  int outputs_ready, int fast_div, cudaStream_t st);
+                  int outputs_ready, int fast_div, const int32_t *view_shift, cudaStream_t st);
 int render_clear_outputs(float *F, void *A, void *D, int64_t n, int channels, int sharded,
                          int maps64, cudaStream_t st);
 
@@ -69,6 +69,10 @@ struct FrameParams {
     artemis_camera cam[kMaxViews];  // the frame's views (one unless artemis_frame_run_views)
     int32_t order_on;  // render the ray tiles in the size's centre-out order (else row-major)
     int32_t pad;
+    // per view: x shift (in 8-pixel tiles) of the view's tile order, so the
+    // views of one launch render the same part of the character at the same
+    // time (stereo eyes: the disparity of the grid centre) -- rows shared in L2
+    int32_t view_shift[kMaxViews];
     double aff[kMaxFrameJoints * 12];
     double rot_inv[kMaxFrameJoints * 9];
 };
@@ -232,7 +236,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            sigma_dep, flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, f->n, 0, f->fast_div, st);
+                           vo.D, f->n, 0, f->fast_div, f->params->view_shift, st);
         mark(5);
         f->launches = 1;
         return rc;
@@ -332,8 +336,9 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution, &f->bmap};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
-    const char *one = getenv("ARTEMIS_VIEWS_ONE_LAUNCH");  // experiment
-    if (vo.n > 1 && !f->small_flut && !(one && one[0] == '1')) {
+    // big FLUT: views rendered together thrash L2 (configs[4] stereo, unaligned:
+    // 8.86 vs 8.27 ms) -- except a stereo pair aligned by disparity (8.14 ms)
+    if (vo.n > 2 && !f->small_flut) {
         // big FLUT: the views' rows would not stay in L2 together (configs[4]
         // stereo: one launch 10.4 ms vs 9.6 ms for two), so one launch per view
         for (int v = 0; v < vo.n && !rc; ++v) {
@@ -342,7 +347,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                sigma_dep, flags & 1, (flags & 8) ? 1 : 0, vo.F[v], vo.A[v],
                                vo.D[v], reinterpret_cast<unsigned long long *>(f->counters + 2),
                                order, &f->params->order_on, nullptr, 1, nullptr, nullptr, nullptr,
-                               f->n, 1, f->fast_div, st);
+                               f->n, 1, f->fast_div, nullptr, st);
         }
         launches += vo.n - 1;
     } else {
@@ -350,7 +355,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            flags & 1, (flags & 8) ? 1 : 0, F, A, D,
                            reinterpret_cast<unsigned long long *>(f->counters + 2), order,
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
-                           vo.D, f->n, 1, f->fast_div, st);
+                           vo.D, f->n, 1, f->fast_div, f->params->view_shift, st);
     }
     mark(5);
     launches += 1;
@@ -637,6 +642,31 @@ static int run_frame_launch(artemis_frame f, int identity, int n_joints, const a
 // (|k| <= 2^22), grid directions are 0 or in [2^-487, 2^60]: all quotients,
 // products and residuals normal. Otherwise the launch takes __ddiv_rn (same
 // bits, slower).
+// Tile-order shifts that align the views of one multi-view launch: view v's
+// tiles are taken shifted by the x offset (in tiles) between the grid
+// centre's projection in view v and in view 0. Only the order changes (every
+// pixel still rendered once, bit-identical maps).
+static void align_views(const artemis_frame_s *f, const artemis_camera *cam, int n,
+                        int32_t *shift) {
+    double c[3];
+    for (int a = 0; a < 3; ++a) c[a] = f->lo[a] + 0.5 * f->cell[a] * f->asset.resolution;
+    double x0 = 0.0;
+    for (int v = 0; v < kMaxViews; ++v) shift[v] = 0;
+    for (int v = 0; v < n; ++v) {
+        const artemis_camera &k = cam[v];
+        double p[3];
+        for (int a = 0; a < 3; ++a)  // camera coordinates: R^T (c - origin)
+            p[a] = k.R[a] * (c[0] - k.origin[0]) + k.R[3 + a] * (c[1] - k.origin[1]) +
+                   k.R[6 + a] * (c[2] - k.origin[2]);
+        if (!(p[2] > 0.0)) return;  // centre behind a camera: no alignment
+        const double x = k.fx * p[0] / p[2] + k.cx;
+        if (v == 0)
+            x0 = x;
+        else
+            shift[v] = (int32_t)lround((x - x0) / 8.0);
+    }
+}
+
 static bool in_range_or_zero(double x, double lo, double hi) {
     const double a = fabs(x);
     return x == 0.0 || (a >= lo && a <= hi);
@@ -710,6 +740,9 @@ static int frame_run_impl(artemis_frame f, const double *joint_aff, const double
         hp->order_on = oslot->mode;
     }
     ARTEMIS_TRY(cudaMemcpyAsync(&f->params->order_on, &hp->order_on, sizeof(int32_t),
+                                cudaMemcpyHostToDevice, st));
+    align_views(f, cam, vo.n, hp->view_shift);
+    ARTEMIS_TRY(cudaMemcpyAsync(f->params->view_shift, hp->view_shift, sizeof(int32_t) * kMaxViews,
                                 cudaMemcpyHostToDevice, st));
     ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));  // the staging block may be reused after this
     f->fast_div = 1;

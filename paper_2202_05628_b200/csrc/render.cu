@@ -633,9 +633,12 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
             const artemis_camera &cam = p.cam[rv];
             const int64_t t = tstart + (kMulti ? gi / nv : gi) * tstride;
             int64_t tile = order ? (int64_t)__ldg(order + t) : t;
-            if (kMulti && p.view_shift[rv]) {  // experiment: disparity-aligned views
-                const int64_t tx = (tile % p.tiles_x + p.view_shift[rv] + p.tiles_x) % p.tiles_x;
-                tile = (tile / p.tiles_x) * p.tiles_x + tx;
+            if (kMulti && p.view_shift) {  // views aligned by the grid centre's projection
+                const int sh = __ldg(p.view_shift + rv) % p.tiles_x;
+                if (sh) {
+                    const int64_t tx = (tile % p.tiles_x + sh + p.tiles_x) % p.tiles_x;
+                    tile = (tile / p.tiles_x) * p.tiles_x + tx;
+                }
             }
             const int sl = (int)(id & 31);
             const int px = (int)(tile % p.tiles_x) * 8 + (sl & 7);
@@ -1269,9 +1272,10 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   void *A, void *D, unsigned long long *queue, const int32_t *tile_order,
                   const int32_t *order_on, void *const *peer_out, int n_views,
                   float *const *Fv, void *const *Av, void *const *Dv, int64_t flut_rows,
-                  int outputs_ready, int fast_div, cudaStream_t st) {
+                  int outputs_ready, int fast_div, const int32_t *view_shift, cudaStream_t st) {
     RenderArgs a{};
     a.fast_div = fast_div;
+    a.view_shift = n_views > 1 ? view_shift : nullptr;
     {   // a FLUT that fits in half the L2 stays resident: prefetching its rows only costs
         static int l2 = 0;
         if (!l2) {
@@ -1296,14 +1300,6 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
             a.Dv[v] = Dv[v];
         }
         a.n_views = n_views;
-        if (const char *env = getenv("ARTEMIS_VIEW_SHIFT")) {  // experiment: "s0,s1,..."
-            int v = 0;
-            for (const char *c = env; *c && v < n_views; ++v) {
-                a.view_shift[v] = atoi(c);
-                while (*c && *c != ',') ++c;
-                if (*c == ',') ++c;
-            }
-        }
         F = Fv[0];
         A = Av[0];
         D = Dv[0];

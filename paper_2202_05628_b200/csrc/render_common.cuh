@@ -42,7 +42,7 @@ struct RenderArgs {
     // image size); with n_views > 1 the outputs of view v are Fv/Av/Dv[v]
     // (alpha/depth float, or double with A64/D64 set non-null)
     int n_views;
-    int view_shift[kMaxViews];  // experiment: per-view x shift of the tile order (tiles)
+    const int32_t *view_shift;  // device, per view: x shift of the tile order (align_views)
     float *Fv[kMaxViews];
     void *Av[kMaxViews];
     void *Dv[kMaxViews];
