@@ -140,20 +140,18 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
         unsigned b = __ballot_sync(0xffffffffu, live && ok);
         if ((threadIdx.x & 31) == 0 && b) atomicAdd(a.n_in, __popc(b));
         if (sizeof(K) == 4 && a.bmask) {
-            // mark the cell in its brick mask (word = key >> 5) and the brick
-            // in the bitmap (word = key >> 14), one atomicOr per distinct word
-            // per warp (lanes hold neighbouring canonical voxels)
+            // mark the cell in its brick mask (word = key >> 5: at most 32
+            // cells, so per-lane atomics barely contend) and the brick in the
+            // bitmap (word = key >> 14: shared by thousands of voxels, so one
+            // atomicOr per distinct brick per warp -- lanes hold neighbouring
+            // canonical voxels)
             const bool on = live && ok;
             const uint32_t key = on ? (uint32_t)morton3((u64)g[0], (u64)g[1], (u64)g[2]) : 0u;
             const int lane = threadIdx.x & 31;
-            const uint32_t mw = on ? key >> 5 : 0xFFFFFFFFu;
-            const unsigned g1 = __match_any_sync(0xffffffffu, mw);
-            const uint32_t m1 = __reduce_or_sync(g1, on ? 1u << (key & 31u) : 0u);
-            if (on && lane == __ffs(g1) - 1) atomicOr(a.bmask + mw, m1);
-            const uint32_t bw = on ? key >> 14 : 0xFFFFFFFFu;
-            const unsigned g2 = __match_any_sync(0xffffffffu, bw);
-            const uint32_t m2 = __reduce_or_sync(g2, on ? 1u << ((key >> 9) & 31u) : 0u);
-            if (on && lane == __ffs(g2) - 1) atomicOr(a.bocc + bw, m2);
+            if (on) atomicOr(a.bmask + (key >> 5), 1u << (key & 31u));
+            const uint32_t brick = on ? key >> 9 : 0xFFFFFFFFu;
+            const unsigned g2 = __match_any_sync(0xffffffffu, brick);
+            if (on && lane == __ffs(g2) - 1) atomicOr(a.bocc + (brick >> 5), 1u << (brick & 31u));
         }
     }
 }
