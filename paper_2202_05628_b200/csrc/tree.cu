@@ -222,6 +222,84 @@ __global__ void pack_tree_kernel(const u64 *__restrict__ codes,
     store_wide(nodes + i, w);
 }
 
+// 32-bit Morton codes (grids up to 2^10 per axis: the frame pipeline) and
+// fewer than 2^30 leaves, reference arrays + leaf records only: the same
+// node-for-node construction as build_node (_core.pyx:193-246) in 32-bit
+// integer arithmetic -- prefix lengths are clz of the 32-bit XOR (the 64-bit
+// lengths minus 32, the same comparisons), indices are int, the bisections
+// compare codes against the split threshold instead of recomputing prefix
+// lengths. The 64-bit build spent most of its issue slots on emulated
+// 64-bit index and bit arithmetic.
+__device__ __forceinline__ uint32_t compact_bits3_32(uint32_t v) {
+    // compact_bits3 restricted to 32-bit inputs (the same masks, truncated)
+    v &= 0x49249249u;
+    v = (v ^ (v >> 2)) & 0xC30C30C3u;
+    v = (v ^ (v >> 4)) & 0x0F00F00Fu;
+    v = (v ^ (v >> 8)) & 0xFF0000FFu;
+    v = (v ^ (v >> 16)) & 0x0000FFFFu;
+    return v;
+}
+
+__global__ void __launch_bounds__(256) build_tree32_kernel(
+    const uint32_t *__restrict__ c, int n_host, const int32_t *__restrict__ n_dev, int32_t *left,
+    int32_t *right, int32_t *bmin, int32_t *bsize, uint4 *leaves,
+    const uint32_t *__restrict__ leaf_flut, const double *__restrict__ sigma,
+    const int32_t *__restrict__ rot_index) {
+    const int n = n_dev ? *n_dev : n_host;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t ci = __ldg(c + i);
+    if (leaves) {
+        const uint32_t row = __ldg(leaf_flut + i);
+        const double sg = sigma ? __ldg(sigma + row) : 0.0;
+        const unsigned long long sb = (unsigned long long)__double_as_longlong(sg);
+        leaves[2 * (size_t)i] =
+            make_uint4(compact_bits3_32(ci), compact_bits3_32(ci >> 1), compact_bits3_32(ci >> 2), row);
+        leaves[2 * (size_t)i + 1] = make_uint4((uint32_t)sb, (uint32_t)(sb >> 32),
+                                               rot_index ? (uint32_t)__ldg(rot_index + row) : 0u, 0u);
+    }
+    if (i >= n - 1) return;
+    // prefix length of codes i and j (-1 outside the array; 32 = equal)
+    auto pl = [&](int j) -> int {
+        if ((unsigned)j >= (unsigned)n) return -1;
+        const uint32_t x = ci ^ __ldg(c + j);
+        return x ? __clz(x) : 32;
+    };
+    const int dir = pl(i + 1) > pl(i - 1) ? 1 : -1;
+    const int floor_len = pl(i - dir);
+    int hi = 2;
+    while (pl(i + hi * dir) > floor_len) hi <<= 1;
+    int len = 0;
+    for (int t = hi >> 1; t >= 1; t >>= 1)
+        if (pl(i + (len + t) * dir) > floor_len) len += t;
+    const int j = i + len * dir;
+    const int first = dir > 0 ? i : j, last = dir > 0 ? j : i;
+    const uint32_t cf = dir > 0 ? ci : __ldg(c + first), cl = dir > 0 ? __ldg(c + last) : ci;
+    // split = the last index sharing more than the range's common prefix with
+    // `first`: the last code below the prefix followed by a 1 bit (the codes
+    // of a range are sorted and share its prefix)
+    const uint32_t x = cf ^ cl;
+    const int fb = x ? 32 - __clz(x) : 0;  // range_free_bits
+    int split = first;
+    if (x) {
+        const uint32_t thr = (cl >> (fb - 1)) << (fb - 1);
+        int step = last - first;
+        do {
+            step = (step + 1) >> 1;
+            if (split + step < last && __ldg(c + split + step) < thr) split += step;
+        } while (step > 1);
+    }  // equal codes (duplicates): no longer prefix exists, split = first
+    left[i] = split == first ? ~split : split;
+    right[i] = split + 1 == last ? ~(split + 1) : split + 1;
+    const uint32_t base = fb >= 32 ? 0u : (cf >> fb) << fb;
+    bmin[3 * i] = (int32_t)compact_bits3_32(base);
+    bmin[3 * i + 1] = (int32_t)compact_bits3_32(base >> 1);
+    bmin[3 * i + 2] = (int32_t)compact_bits3_32(base >> 2);
+    bsize[3 * i] = box_size_axis(fb, 0);
+    bsize[3 * i + 1] = box_size_axis(fb, 1);
+    bsize[3 * i + 2] = box_size_axis(fb, 2);
+}
+
 template <typename K>
 int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int64_t n_cap,
                       int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
@@ -230,6 +308,12 @@ int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int6
                       cudaStream_t st) {
     int64_t threads = n_cap > 1 ? n_cap : 1;
     int blocks = (int)ceil_div<int64_t>(threads, 256);
+    if (sizeof(K) == 4 && !nodes && !dup_flag && left && n_cap < (int64_t(1) << 30)) {
+        build_tree32_kernel<<<blocks, 256, 0, st>>>(
+            reinterpret_cast<const uint32_t *>(codes), (int)n_host, n_dev, left, right, bmin,
+            bsize, leaves, leaf_flut, sigma, rot_index);
+        return ARTEMIS_LAUNCHED();
+    }
     build_tree_kernel<K><<<blocks, 256, 0, st>>>(codes, n_host, n_dev, left, right, bmin, bsize,
                                                   nodes, leaves, leaf_flut, sigma, rot_index,
                                                   dup_flag);
