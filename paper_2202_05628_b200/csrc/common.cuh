@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "artemis.h"
 
@@ -43,6 +44,49 @@ int check_launch();  // ARTEMIS_OK or ARTEMIS_ERR_CUDA after a launch
     } while (0)
 
 #define ARTEMIS_LAUNCHED() ::artemis::check_launch()
+
+// ---- programmatic dependent launch ------------------------------------------
+// The frame's kernel chain (counting rebuild -> Karras build -> finish ->
+// render) is launched with programmatic stream serialization: the next grid
+// is scheduled while the previous one drains (once all of its blocks have
+// called griddep_launch_dependents or exited) instead of after a full
+// launch round trip. A kernel launched this way MUST call griddep_wait()
+// before its first access to memory an earlier launch wrote; both are no-ops
+// for a normal launch. ARTEMIS_PDL=0 launches them normally (A/B).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("ARTEMIS_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess) {
+        set_cuda_error(e);
+        return ARTEMIS_ERR_CUDA;
+    }
+    return check_launch();
+}
 
 inline cudaStream_t S(artemis_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 

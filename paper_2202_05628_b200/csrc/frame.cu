@@ -43,6 +43,7 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
                      BrickRec *recs, int32_t *table, const int dims[3], int32_t *aabb,
                      uint32_t *live_codes, uint32_t *winners, unsigned long long *wkey,
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches);
+int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st);
 int counting_finish(const int32_t *n_live, uint32_t *widx, unsigned long long *wkey,
                     uint32_t *winners, cudaStream_t st);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
@@ -257,6 +258,10 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                                       vo.n > 1 ? 0 : sharded, (flags & 8) ? 1 : 0, f->side);
             if (rc) return rc;
         }
+    }
+    if (f->counting) {
+        rc = counting_prepare(f->btable, f->bdims, f->bmeta + 1, st);
+        if (rc) return rc;
     }
     rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,
                        identity ? 1 : n_joints, f->lo, f->cell, as.resolution, f->key_bytes,
@@ -710,20 +715,13 @@ static int frame_run_impl(artemis_frame f, const double *joint_aff, const double
     FrameParams *hp = f->staging + sidx;
     ARTEMIS_TRY(cudaEventSynchronize(f->staged[sidx]));  // its last copy has completed
     for (int v = 0; v < vo.n; ++v) hp->cam[v] = cam[v];
-    ARTEMIS_TRY(cudaMemcpyAsync(f->params->cam, hp->cam, sizeof(artemis_camera) * vo.n,
-                                cudaMemcpyHostToDevice, st));
+    const int nj = identity ? 1 : n_joints;
     if (identity) {
         static const double eye[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
         memcpy(hp->rot_inv, eye, sizeof(eye));
-        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, hp->rot_inv, sizeof(eye),
-                                    cudaMemcpyHostToDevice, st));
     } else {
         memcpy(hp->aff, joint_aff, sizeof(double) * 12 * n_joints);
         memcpy(hp->rot_inv, rot_inv, sizeof(double) * 9 * n_joints);
-        ARTEMIS_TRY(cudaMemcpyAsync(f->params->aff, hp->aff, sizeof(double) * 12 * n_joints,
-                                    cudaMemcpyHostToDevice, st));
-        ARTEMIS_TRY(cudaMemcpyAsync(f->params->rot_inv, hp->rot_inv,
-                                    sizeof(double) * 9 * n_joints, cudaMemcpyHostToDevice, st));
     }
     const int sharded = cam->tile_stride > 1;
     if (sharded && f->peer_out[0] &&
@@ -739,11 +737,11 @@ static int frame_run_impl(artemis_frame f, const double *joint_aff, const double
         order = oslot->dev;
         hp->order_on = oslot->mode;
     }
-    ARTEMIS_TRY(cudaMemcpyAsync(&f->params->order_on, &hp->order_on, sizeof(int32_t),
-                                cudaMemcpyHostToDevice, st));
     align_views(f, cam, vo.n, hp->view_shift);
-    ARTEMIS_TRY(cudaMemcpyAsync(f->params->view_shift, hp->view_shift, sizeof(int32_t) * kMaxViews,
-                                cudaMemcpyHostToDevice, st));
+    // one host -> device copy of the block's used prefix (cameras, order
+    // switch, view shifts, joint tables up to the last used rotation)
+    const size_t used = offsetof(FrameParams, rot_inv) + sizeof(double) * 9 * nj;
+    ARTEMIS_TRY(cudaMemcpyAsync(f->params, hp, used, cudaMemcpyHostToDevice, st));
     ARTEMIS_TRY(cudaEventRecord(f->staged[sidx], st));  // the staging block may be reused after this
     f->fast_div = 1;
     for (int v = 0; v < vo.n; ++v)

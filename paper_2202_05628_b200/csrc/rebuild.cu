@@ -97,6 +97,8 @@ __global__ void count_kernel(const uint32_t *__restrict__ bocc,
                              uint32_t *__restrict__ n_bricks, uint32_t *__restrict__ n_cells,
                              uint32_t *__restrict__ bpre, uint32_t *__restrict__ blk_bricks,
                              uint32_t *__restrict__ blk_cells, int32_t *aabb) {
+    griddep_wait();
+    griddep_launch_dependents();
     __shared__ int red[6][kCountThreads / 32];
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -181,6 +183,8 @@ __global__ void count_kernel(const uint32_t *__restrict__ bocc,
 // exclusive scans of both count arrays (one block), totals to n_live / n_recs
 __global__ void __launch_bounds__(1024) scan2_kernel(uint32_t *a, uint32_t *b, int64_t n,
                                                      int32_t *total_b, int32_t *total_a) {
+    griddep_wait();
+    griddep_launch_dependents();
     __shared__ uint32_t sa[32], sb[32];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int64_t per = (n + 1023) / 1024;
@@ -266,6 +270,8 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
                             const uint32_t *__restrict__ blk_cells,
                             const uint32_t *__restrict__ bpre, BrickRec *__restrict__ recs,
                             int32_t *__restrict__ table, int dx, int dy) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= n_words) return;
@@ -310,6 +316,8 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
 __global__ void finish_kernel(const int32_t *__restrict__ n_live, uint32_t *__restrict__ widx,
                               unsigned long long *__restrict__ wkey,
                               uint32_t *__restrict__ winners) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t n = *n_live;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -321,8 +329,7 @@ __global__ void finish_kernel(const int32_t *__restrict__ n_live, uint32_t *__re
 
 int counting_finish(const int32_t *n_live, uint32_t *widx, unsigned long long *wkey,
                     uint32_t *winners, cudaStream_t st) {
-    finish_kernel<<<num_sms() * 4, 256, 0, st>>>(n_live, widx, wkey, winners);
-    return ARTEMIS_LAUNCHED();
+    return launch_pdl(finish_kernel, num_sms() * 4, 256, 0, st, n_live, widx, wkey, winners);
 }
 
 // live-cell rank of an in-bounds voxel's key (from its brick record)
@@ -343,6 +350,8 @@ __global__ void slot_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32
                             uint32_t *__restrict__ live_codes,
                             unsigned long long *__restrict__ wkey, uint32_t *__restrict__ bocc,
                             int64_t n_words) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n_words) bocc[i] = 0u;  // emit has read the bitmap: clear it for the next frame
     if (i >= n) return;
@@ -359,6 +368,8 @@ __global__ void winner_kernel(const uint32_t *__restrict__ keys, int64_t n, uint
                               const BrickRec *__restrict__ recs, int dx, int dy,
                               const unsigned long long *__restrict__ wkey,
                               uint32_t *__restrict__ widx) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = keys[i];
@@ -377,23 +388,36 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches) {
     uint32_t *nb = wtmp, *nc = wtmp + n_words;
     const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
-    ARTEMIS_TRY(cudaMemsetAsync(table, 0xFF, cells * sizeof(int32_t), st));
-    ARTEMIS_TRY(cudaMemsetAsync(aabb, 0x7F, 3 * sizeof(int32_t), st));
-    ARTEMIS_TRY(cudaMemsetAsync(aabb + 3, 0x80, 3 * sizeof(int32_t), st));
+    (void)cells;  // the table and AABB were reset by counting_prepare
     const int wb = (int)ceil_div<int64_t>(n_words * 32, kCountThreads);
     uint32_t *bpre = wtmp + 2 * n_words;  // per dense brick: cells before it in its word
     uint32_t *bb = bpre + 32 * n_words, *bc = bb + wb;  // per count block: bricks, cells
-    count_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bpre, bb, bc, aabb);
-    scan2_kernel<<<1, 1024, 0, st>>>(bc, bb, wb, n_recs, n_live);
-    emit_kernel<<<wb, kCountThreads, 0, st>>>(bocc, bmask, n_words, nb, nc, bb, bc, bpre, recs,
-                                              table, dims[0], dims[1]);
+    int rc = launch_pdl(count_kernel, wb, kCountThreads, 0, st, bocc, bmask, n_words, nb, nc,
+                        bpre, bb, bc, aabb);
+    if (rc) return rc;
+    rc = launch_pdl(scan2_kernel, 1, 1024, 0, st, bc, bb, (int64_t)wb, n_recs, n_live);
+    if (rc) return rc;
+    rc = launch_pdl(emit_kernel, wb, kCountThreads, 0, st, bocc, bmask, n_words, nb, nc, bb, bc,
+                    bpre, recs, table, dims[0], dims[1]);
+    if (rc) return rc;
     const int vb = (int)ceil_div<int64_t>(std::max<int64_t>(n, n_words), kCountThreads);
-    slot_kernel<<<vb, kCountThreads, 0, st>>>(keys, n, sentinel, sigma, table, recs, dims[0],
-                                              dims[1], live_codes, wkey, bocc, n_words);
-    winner_kernel<<<(int)ceil_div<int64_t>(n, kCountThreads), kCountThreads, 0, st>>>(
-        keys, n, sentinel, sigma, table, recs, dims[0], dims[1], wkey, winners);
+    rc = launch_pdl(slot_kernel, vb, kCountThreads, 0, st, keys, n, sentinel, sigma, table, recs,
+                    dims[0], dims[1], live_codes, wkey, bocc, n_words);
+    if (rc) return rc;
+    rc = launch_pdl(winner_kernel, (int)ceil_div<int64_t>(n, kCountThreads), kCountThreads, 0, st,
+                    keys, n, sentinel, sigma, table, recs, dims[0], dims[1], wkey, winners);
     if (launches) *launches += 5;
-    return ARTEMIS_LAUNCHED();
+    return rc;
+}
+
+// Before the warp kernel (so the kernel chain after it has no memset nodes
+// between its launches): the dense brick table and the leaf AABB reset.
+int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st) {
+    const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
+    ARTEMIS_TRY(cudaMemsetAsync(table, 0xFF, cells * sizeof(int32_t), st));
+    ARTEMIS_TRY(cudaMemsetAsync(aabb, 0x7F, 3 * sizeof(int32_t), st));
+    ARTEMIS_TRY(cudaMemsetAsync(aabb + 3, 0x80, 3 * sizeof(int32_t), st));
+    return ARTEMIS_OK;
 }
 
 }  // namespace artemis

@@ -312,6 +312,7 @@ __device__ __forceinline__ bool hit_filtered(uint32_t w0, uint32_t w1, uint32_t 
 // 3 / 4 = as 1 / 2 over several views in one launch (run_views)
 template <int kDeg, int kMode, int kRays, bool kVec, bool kDDA, bool kFast>
 __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_kernel(RenderArgs p) {
+    griddep_wait();  // launched as a dependent of the frame's last rebuild kernel
     constexpr bool kCamera = kRays != 0;
     constexpr bool kMulti = kRays >= 3;  // several views per launch (run_views)
     constexpr int H = (kDeg + 1) * (kDeg + 1);
@@ -1156,6 +1157,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
                         (size_t)kRenderWarps * 32 * kQCap * (2 + 4) + (size_t)kRenderThreads * 6 * 8 +
                         (kDDA && ARTEMIS_SMEM_MASK ? (size_t)kRenderThreads * 64 : 0);
     const int64_t want = ceil_div<int64_t>(warps, kRenderWarps);
+    int rc_launch = ARTEMIS_OK;
     switch (degree) {
 #define ARTEMIS_LAUNCH(D)                                                                       \
     case D: {                                                                                   \
@@ -1166,7 +1168,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRenderThreads, smem);        \
         int blocks = (int)std::min<int64_t>(want, (int64_t)num_sms() * (occ > 0 ? occ : 1)); \
         if (g_render_block_cap > 0 && blocks > g_render_block_cap) blocks = g_render_block_cap; \
-        kern<<<blocks, kRenderThreads, smem, st>>>(a);                                          \
+        rc_launch = launch_pdl(kern, blocks, kRenderThreads, smem, st, a);                     \
         break;                                                                                  \
     }
         ARTEMIS_LAUNCH(0) ARTEMIS_LAUNCH(1) ARTEMIS_LAUNCH(2) ARTEMIS_LAUNCH(3) ARTEMIS_LAUNCH(4)
@@ -1174,7 +1176,7 @@ int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream
         default:
             return ARTEMIS_ERR_ARG;
     }
-    return ARTEMIS_LAUNCHED();
+    return rc_launch;
 }
 
 template <int kMode, int kRays>

@@ -245,6 +245,8 @@ __global__ void __launch_bounds__(256) build_tree32_kernel(
     int32_t *right, int32_t *bmin, int32_t *bsize, uint4 *leaves,
     const uint32_t *__restrict__ leaf_flut, const double *__restrict__ sigma,
     const int32_t *__restrict__ rot_index) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int n = n_dev ? *n_dev : n_host;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -309,10 +311,9 @@ int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int6
     int64_t threads = n_cap > 1 ? n_cap : 1;
     int blocks = (int)ceil_div<int64_t>(threads, 256);
     if (sizeof(K) == 4 && !nodes && !dup_flag && left && n_cap < (int64_t(1) << 30)) {
-        build_tree32_kernel<<<blocks, 256, 0, st>>>(
-            reinterpret_cast<const uint32_t *>(codes), (int)n_host, n_dev, left, right, bmin,
-            bsize, leaves, leaf_flut, sigma, rot_index);
-        return ARTEMIS_LAUNCHED();
+        return launch_pdl(build_tree32_kernel, blocks, 256, 0, st,
+                          reinterpret_cast<const uint32_t *>(codes), (int)n_host, n_dev, left,
+                          right, bmin, bsize, leaves, leaf_flut, sigma, rot_index);
     }
     build_tree_kernel<K><<<blocks, 256, 0, st>>>(codes, n_host, n_dev, left, right, bmin, bsize,
                                                   nodes, leaves, leaf_flut, sigma, rot_index,
