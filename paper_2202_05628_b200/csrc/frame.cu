@@ -41,11 +41,11 @@ int warp_pipeline(const int32_t *cells, int64_t n, int slots, const int32_t *jid
 int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const double *sigma,
                      uint32_t *bocc, uint32_t *bmask, int64_t n_words, uint32_t *wtmp,
                      BrickRec *recs, int32_t *table, const int dims[3], int32_t *aabb,
-                     uint32_t *live_codes, uint32_t *winners, unsigned long long *wkey,
+                     uint32_t *live_codes, unsigned long long *wmax,
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches);
 int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st);
-int counting_finish(const int32_t *n_live, uint32_t *widx, unsigned long long *wkey,
-                    uint32_t *winners, cudaStream_t st);
+int counting_finish(const int32_t *n_live, unsigned long long *wmax, uint32_t *winners,
+                    cudaStream_t st);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
@@ -105,8 +105,8 @@ struct artemis_frame_s {
     int counting = 0;
     uint32_t *bmask = nullptr, *bocc = nullptr, *wtmp = nullptr;
     int64_t n_words = 0;
+    // per live slot: 128-bit max of (density key, ~index), kept reset between frames
     unsigned long long *wkey = nullptr;
-    uint32_t *widx = nullptr;  // atomicMin scratch of the winners (kept reset between frames)
     void *sort_ws = nullptr, *resolve_ws = nullptr;
     size_t sort_ws_bytes = 0, resolve_ws_bytes = 0;
     FrameParams *params = nullptr;
@@ -275,19 +275,19 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         // sort (rebuild.cu), the brick map in the same passes
         rc = counting_rebuild((const uint32_t *)f->keys, f->n, (uint32_t)f->sentinel, as.sigma,
                               f->bocc, f->bmask, f->n_words, f->wtmp, f->brecs, f->btable,
-                              f->bdims, f->bmeta + 1, (uint32_t *)f->live_codes, f->widx,
+                              f->bdims, f->bmeta + 1, (uint32_t *)f->live_codes,
                               f->wkey, f->counters + 1, f->bmeta, st, &launches);
         if (rc) return rc;
         mark(2);
+        rc = counting_finish(f->counters + 1, f->wkey, f->winners, st);
+        if (rc) return rc;
         mark(3);
         rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
                                          f->n, f->left, f->right, f->bmin, f->bsize, nullptr,
-                                         f->leaves, f->widx, as.sigma, f->rot_joint, nullptr,
+                                         f->leaves, f->winners, as.sigma, f->rot_joint, nullptr,
                                          st);
         if (rc) return rc;
-        rc = counting_finish(f->counters + 1, f->widx, f->wkey, f->winners, st);
-        if (rc) return rc;
-        launches += 2;  // the Karras build, finish (count/scan/emit/slot/winner counted above)
+        launches += 2;  // finish, the Karras build (count/scan/emit/slot counted above)
         // the side stream only cleared the outputs: join it before the render
         ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));
         ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
@@ -563,12 +563,10 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
         rc = rc ? rc : dev_alloc(&f->bmask, (size_t)f->n_words * 32 * 16 * 4);
         rc = rc ? rc : dev_alloc(&f->bocc, (size_t)f->n_words * 4);
         rc = rc ? rc : dev_alloc(&f->wtmp, (size_t)f->n_words * (8 + 32 * 4 + 8));
-        rc = rc ? rc : dev_alloc(&f->wkey, (size_t)n * 8);
-        rc = rc ? rc : dev_alloc(&f->widx, (size_t)n * 4);
+        rc = rc ? rc : dev_alloc(&f->wkey, (size_t)n * 16);
         if (!rc && (cudaMemset(f->bmask, 0, (size_t)f->n_words * 32 * 16 * 4) != cudaSuccess ||
                     cudaMemset(f->bocc, 0, (size_t)f->n_words * 4) != cudaSuccess ||
-                    cudaMemset(f->wkey, 0, (size_t)n * 8) != cudaSuccess ||
-                    cudaMemset(f->widx, 0xFF, (size_t)n * 4) != cudaSuccess))
+                    cudaMemset(f->wkey, 0, (size_t)n * 16) != cudaSuccess))
             rc = ARTEMIS_ERR_CUDA;
     }
     if (!rc) {
@@ -621,8 +619,7 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     void *bufs[] = {f->keys, f->keys_sorted, f->live_codes, f->vals, f->vals_sorted, f->winners,
                     f->rot_joint, f->counters, f->left, f->right, f->bmin, f->bsize, f->nodes,
                     f->leaves, f->btable, f->brecs, f->bmeta,
-                    f->sort_ws, f->resolve_ws, f->params, f->bmask, f->bocc, f->wtmp, f->wkey,
-                    f->widx};
+                    f->sort_ws, f->resolve_ws, f->params, f->bmask, f->bocc, f->wtmp, f->wkey};
     for (void *b : bufs)
         if (b) cudaFree(b);
     delete f;

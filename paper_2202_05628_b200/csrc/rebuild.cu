@@ -21,12 +21,12 @@
 //                 per-word prefix, first leaf), the dense brick table entry,
 //                 the leaf-cell AABB; clears the dense masks for the next frame
 //   slot          per in-bounds voxel: its live-cell rank = record.first +
-//                 prefix + popc(mask below the bit); live code; atomicMax of
-//                 the density's total-order key
-//   winner        per in-bounds voxel holding the maximal key: atomicMin of
-//                 its canonical index -> the winner
-// Integer atomics (or / max / min) commute, so the result is deterministic
-// and equals the reference's order, with no per-entry sort at all.
+//                 prefix + popc(mask below the bit); live code; 128-bit
+//                 atomic max of (density total-order key, ~index) -> the
+//                 winner (largest density, then lowest index)
+//   finish        winners out of the max scratch, scratch reset
+// Integer atomics (or / max) commute, so the result is deterministic and
+// equals the reference's order, with no per-entry sort at all.
 #include <algorithm>
 
 #include "bricks.cuh"
@@ -310,26 +310,25 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
     table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
 }
 
-// after the Karras build consumed them: the winners out of the atomicMin
-// scratch into the frame's winner array, and the scratch slots the frame
-// used reset for the next frame
-__global__ void finish_kernel(const int32_t *__restrict__ n_live, uint32_t *__restrict__ widx,
-                              unsigned long long *__restrict__ wkey,
+// the winners out of the 128-bit max scratch (low word = 2^32 - 1 - index)
+// into the frame's winner array, and the scratch slots the frame used reset
+// for the next frame (a zero entry loses to every voxel)
+__global__ void finish_kernel(const int32_t *__restrict__ n_live, ulonglong2 *__restrict__ wmax,
                               uint32_t *__restrict__ winners) {
     griddep_wait();
     griddep_launch_dependents();
     const int64_t n = *n_live;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        winners[i] = widx[i];
-        widx[i] = 0xFFFFFFFFu;
-        wkey[i] = 0ull;
+        winners[i] = 0xFFFFFFFFu - (uint32_t)wmax[i].x;
+        wmax[i] = make_ulonglong2(0ull, 0ull);
     }
 }
 
-int counting_finish(const int32_t *n_live, uint32_t *widx, unsigned long long *wkey,
-                    uint32_t *winners, cudaStream_t st) {
-    return launch_pdl(finish_kernel, num_sms() * 4, 256, 0, st, n_live, widx, wkey, winners);
+int counting_finish(const int32_t *n_live, unsigned long long *wmax, uint32_t *winners,
+                    cudaStream_t st) {
+    return launch_pdl(finish_kernel, num_sms() * 4, 256, 0, st, n_live,
+                      reinterpret_cast<ulonglong2 *>(wmax), winners);
 }
 
 // live-cell rank of an in-bounds voxel's key (from its brick record)
@@ -344,12 +343,26 @@ __device__ __forceinline__ uint32_t live_rank(uint32_t key, const int32_t *__res
     return R.first + R.prefix[q] + (uint32_t)__popc(R.mask[q] & ((1u << (l & 31u)) - 1u));
 }
 
+// 128-bit atomic max of (density key, 2^32 - 1 - index): the winner rule in
+// one pass -- largest density first, ties to the lowest canonical index
+// (_core / rigging.py:435 lexsort order). A compare-and-swap loop; most
+// cells hold one voxel, so most slots take one CAS.
+__device__ __forceinline__ void winner_max(ulonglong2 *slot, unsigned long long key, uint32_t i) {
+    unsigned __int128 *p = reinterpret_cast<unsigned __int128 *>(slot);
+    const unsigned __int128 v = ((unsigned __int128)key << 64) | (unsigned __int128)(0xFFFFFFFFu - i);
+    unsigned __int128 cur = *p;
+    while (cur < v) {
+        const unsigned __int128 seen = atomicCAS(p, cur, v);
+        if (seen == cur) break;
+        cur = seen;
+    }
+}
+
 __global__ void slot_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32_t sentinel,
                             const double *__restrict__ sigma, const int32_t *__restrict__ table,
                             const BrickRec *__restrict__ recs, int dx, int dy,
-                            uint32_t *__restrict__ live_codes,
-                            unsigned long long *__restrict__ wkey, uint32_t *__restrict__ bocc,
-                            int64_t n_words) {
+                            uint32_t *__restrict__ live_codes, ulonglong2 *__restrict__ wmax,
+                            uint32_t *__restrict__ bocc, int64_t n_words) {
     griddep_wait();
     griddep_launch_dependents();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -359,23 +372,7 @@ __global__ void slot_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32
     if (key == sentinel) return;
     const uint32_t s = live_rank(key, table, recs, dx, dy);
     live_codes[s] = key;  // every voxel of the cell writes the same code
-    atomicMax(wkey + s, density_key(sigma[i]));
-}
-
-__global__ void winner_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32_t sentinel,
-                              const double *__restrict__ sigma,
-                              const int32_t *__restrict__ table,
-                              const BrickRec *__restrict__ recs, int dx, int dy,
-                              const unsigned long long *__restrict__ wkey,
-                              uint32_t *__restrict__ widx) {
-    griddep_wait();
-    griddep_launch_dependents();
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t key = keys[i];
-    if (key == sentinel) return;
-    const uint32_t s = live_rank(key, table, recs, dx, dy);
-    if (density_key(sigma[i]) == wkey[s]) atomicMin(widx + s, (uint32_t)i);
+    winner_max(wmax + s, density_key(sigma[i]), (uint32_t)i);
 }
 
 // The counting rebuild after the warp kernel marked bmask / bocc: leaves
@@ -384,7 +381,7 @@ __global__ void winner_kernel(const uint32_t *__restrict__ keys, int64_t n, uint
 int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const double *sigma,
                      uint32_t *bocc, uint32_t *bmask, int64_t n_words, uint32_t *wtmp,
                      BrickRec *recs, int32_t *table, const int dims[3], int32_t *aabb,
-                     uint32_t *live_codes, uint32_t *winners, unsigned long long *wkey,
+                     uint32_t *live_codes, unsigned long long *wmax,
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches) {
     uint32_t *nb = wtmp, *nc = wtmp + n_words;
     const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
@@ -402,11 +399,9 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
     if (rc) return rc;
     const int vb = (int)ceil_div<int64_t>(std::max<int64_t>(n, n_words), kCountThreads);
     rc = launch_pdl(slot_kernel, vb, kCountThreads, 0, st, keys, n, sentinel, sigma, table, recs,
-                    dims[0], dims[1], live_codes, wkey, bocc, n_words);
-    if (rc) return rc;
-    rc = launch_pdl(winner_kernel, (int)ceil_div<int64_t>(n, kCountThreads), kCountThreads, 0, st,
-                    keys, n, sentinel, sigma, table, recs, dims[0], dims[1], wkey, winners);
-    if (launches) *launches += 5;
+                    dims[0], dims[1], live_codes, reinterpret_cast<ulonglong2 *>(wmax), bocc,
+                    n_words);
+    if (launches) *launches += 4;
     return rc;
 }
 
