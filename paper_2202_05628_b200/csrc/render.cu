@@ -51,7 +51,8 @@ namespace artemis {
 #define ARTEMIS_DEDUP 1
 #endif
 #ifndef ARTEMIS_ROW_PREFETCH
-#define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line, 3 into L1
+#define ARTEMIS_ROW_PREFETCH 1  // 0 none, 1 every 128-B line of a queued row, 2 first line, 3 into L1,
+                                // 4 one bulk (cp.async.bulk.prefetch.L2) per row
 #endif
 namespace {
 constexpr int kRenderWarps = 4;
@@ -835,6 +836,14 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #if ARTEMIS_ROW_PREFETCH
                 if (!p.no_row_prefetch) {  // the row's 9 x 128 B lines are read in phase C
                     const char *row = reinterpret_cast<const char *>(p.coef + (size_t)fidx * p.coef_stride);
+#if ARTEMIS_ROW_PREFETCH == 4
+                    // one bulk (TMA-engine) L2 prefetch of the whole row: vec rows are
+                    // 16-B aligned with a multiple-of-16 length
+                    if (kVec) {
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row),
+                                     "r"((unsigned)(p.coef_stride * 4)));
+                    } else
+#endif
                     for (int off = 0; off < (ARTEMIS_ROW_PREFETCH == 2 ? 1 : p.coef_stride * 4); off += 128) {
 #if ARTEMIS_ROW_PREFETCH == 3
                         asm volatile("prefetch.global.L1 [%0];" ::"l"(row + off));

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
         if (kPipeline) {
             K key = ok ? (K)morton3((u64)g[0], (u64)g[1], (u64)g[2]) : (K)a.sentinel;
             reinterpret_cast<K *>(a.keys)[i] = key;
-            a.vals[i] = (uint32_t)i;
+            if (!a.bmask) a.vals[i] = (uint32_t)i;  // sort values (the counting rebuild has none)
         }
     }
     if (kPipeline) {
