@@ -44,6 +44,8 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
                      uint32_t *live_codes, unsigned long long *wmax,
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches);
 int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st);
+int counting_finish(const int32_t *n_live, unsigned long long *wmax, uint32_t *winners,
+                    cudaStream_t st);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
@@ -277,14 +279,15 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                               f->wkey, f->counters + 1, f->bmeta, st, &launches);
         if (rc) return rc;
         mark(2);
-        // the Karras build takes the winners out of the slot pass's max
-        // scratch (and resets it) as it writes the leaf records
-        mark(3);
-        rc = launch_build_tree32_winners((const uint32_t *)f->live_codes, f->counters + 1, f->n,
-                                         f->left, f->right, f->bmin, f->bsize, f->leaves,
-                                         f->wkey, f->winners, as.sigma, f->rot_joint, st);
+        rc = counting_finish(f->counters + 1, f->wkey, f->winners, st);
         if (rc) return rc;
-        launches += 1;  // the Karras build (count/scan/emit/slot counted above)
+        mark(3);
+        rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
+                                         f->n, f->left, f->right, f->bmin, f->bsize, nullptr,
+                                         f->leaves, f->winners, as.sigma, f->rot_joint, nullptr,
+                                         st);
+        if (rc) return rc;
+        launches += 2;  // finish, the Karras build (count/scan/emit/slot counted above)
         // the side stream only cleared the outputs: join it before the render
         ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));
         ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));

@@ -24,8 +24,7 @@
 //                 prefix + popc(mask below the bit); live code; 128-bit
 //                 atomic max of (density total-order key, ~index) -> the
 //                 winner (largest density, then lowest index)
-//   (Karras build) takes the winners out of the max scratch and resets it
-//                 (tree.cu, launch_build_tree32_winners)
+//   finish        winners out of the max scratch, scratch reset
 // Integer atomics (or / max) commute, so the result is deterministic and
 // equals the reference's order, with no per-entry sort at all.
 #include <algorithm>
@@ -309,6 +308,27 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
     const int bx = (int)compact_bits3(b), by = (int)compact_bits3(b >> 1),
               bz = (int)compact_bits3(b >> 2);
     table[((size_t)bz * dy + by) * dx + bx] = (int32_t)rec;
+}
+
+// the winners out of the 128-bit max scratch (low word = 2^32 - 1 - index)
+// into the frame's winner array, and the scratch slots the frame used reset
+// for the next frame (a zero entry loses to every voxel)
+__global__ void finish_kernel(const int32_t *__restrict__ n_live, ulonglong2 *__restrict__ wmax,
+                              uint32_t *__restrict__ winners) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int64_t n = *n_live;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        winners[i] = 0xFFFFFFFFu - (uint32_t)wmax[i].x;
+        wmax[i] = make_ulonglong2(0ull, 0ull);
+    }
+}
+
+int counting_finish(const int32_t *n_live, unsigned long long *wmax, uint32_t *winners,
+                    cudaStream_t st) {
+    return launch_pdl(finish_kernel, num_sms() * 4, 256, 0, st, n_live,
+                      reinterpret_cast<ulonglong2 *>(wmax), winners);
 }
 
 // live-cell rank of an in-bounds voxel's key (from its brick record)

@@ -244,8 +244,7 @@ __global__ void __launch_bounds__(256) build_tree32_kernel(
     const uint32_t *__restrict__ c, int n_host, const int32_t *__restrict__ n_dev, int32_t *left,
     int32_t *right, int32_t *bmin, int32_t *bsize, uint4 *leaves,
     const uint32_t *__restrict__ leaf_flut, const double *__restrict__ sigma,
-    const int32_t *__restrict__ rot_index, ulonglong2 *__restrict__ wmax,
-    uint32_t *__restrict__ winners) {
+    const int32_t *__restrict__ rot_index) {
     griddep_wait();
     griddep_launch_dependents();
     const int n = n_dev ? *n_dev : n_host;
@@ -253,17 +252,7 @@ __global__ void __launch_bounds__(256) build_tree32_kernel(
     if (i >= n) return;
     const uint32_t ci = __ldg(c + i);
     if (leaves) {
-        uint32_t row;
-        if (wmax) {
-            // counting rebuild: the leaf's winner out of the 128-bit max scratch
-            // (low word = 2^32 - 1 - index), the slot reset for the next frame
-            // (rebuild.cu; was a separate finish pass)
-            row = 0xFFFFFFFFu - (uint32_t)wmax[i].x;
-            wmax[i] = make_ulonglong2(0ull, 0ull);
-            winners[i] = row;
-        } else {
-            row = __ldg(leaf_flut + i);
-        }
+        const uint32_t row = __ldg(leaf_flut + i);
         const double sg = sigma ? __ldg(sigma + row) : 0.0;
         const unsigned long long sb = (unsigned long long)__double_as_longlong(sg);
         leaves[2 * (size_t)i] =
@@ -324,25 +313,12 @@ int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int6
     if (sizeof(K) == 4 && !nodes && !dup_flag && left && n_cap < (int64_t(1) << 30)) {
         return launch_pdl(build_tree32_kernel, blocks, 256, 0, st,
                           reinterpret_cast<const uint32_t *>(codes), (int)n_host, n_dev, left,
-                          right, bmin, bsize, leaves, leaf_flut, sigma, rot_index,
-                          (ulonglong2 *)nullptr, (uint32_t *)nullptr);
+                          right, bmin, bsize, leaves, leaf_flut, sigma, rot_index);
     }
     build_tree_kernel<K><<<blocks, 256, 0, st>>>(codes, n_host, n_dev, left, right, bmin, bsize,
                                                   nodes, leaves, leaf_flut, sigma, rot_index,
                                                   dup_flag);
     return ARTEMIS_LAUNCHED();
-}
-
-// Frame pipeline, counting rebuild: the Karras build also takes the winners
-// out of the slot pass's max scratch (and resets it) -- one pass fewer.
-int launch_build_tree32_winners(const uint32_t *codes, const int32_t *n_dev, int64_t n_cap,
-                                int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
-                                uint4 *leaves, unsigned long long *wmax, uint32_t *winners,
-                                const double *sigma, const int32_t *rot_index, cudaStream_t st) {
-    const int blocks = (int)ceil_div<int64_t>(n_cap > 1 ? n_cap : 1, 256);
-    return launch_pdl(build_tree32_kernel, blocks, 256, 0, st, codes, 0, n_dev, left, right,
-                      bmin, bsize, leaves, (const uint32_t *)nullptr, sigma, rot_index,
-                      reinterpret_cast<ulonglong2 *>(wmax), winners);
 }
 
 template int launch_build_tree<u64>(const u64 *, int64_t, const int32_t *, int64_t, int32_t *,

@@ -10,10 +10,6 @@ int launch_build_tree(const K *codes, int64_t n_host, const int32_t *n_dev, int6
                       WideNode *nodes, uint4 *leaves, const uint32_t *leaf_flut,
                       const double *sigma, const int32_t *rot_index, int32_t *dup_flag,
                       cudaStream_t st);
-int launch_build_tree32_winners(const uint32_t *codes, const int32_t *n_dev, int64_t n_cap,
-                                int32_t *left, int32_t *right, int32_t *bmin, int32_t *bsize,
-                                uint4 *leaves, unsigned long long *wmax, uint32_t *winners,
-                                const double *sigma, const int32_t *rot_index, cudaStream_t st);
 
 // Stable onesweep sort of (key, value) pairs; see sort.cu.
 size_t sort_workspace_bytes(int64_t n, int key_bits, int key_bytes);

@@ -56,15 +56,29 @@ struct WarpArgs {
 template <typename K, bool kPipeline>
 __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
     __shared__ double s_aff[kMaxJoints * 12];
-    if (!a.identity)
-        for (int i = threadIdx.x; i < a.n_joints * 12; i += blockDim.x) s_aff[i] = a.aff[i];
-    __syncthreads();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool live = i < a.n;
+    // the voxel's own rows are loaded before the joint table is staged, so
+    // their latency overlaps the staging and the barrier
+    int32_t ci[3] = {0, 0, 0};
+    int4 jj = make_int4(-1, -1, -1, -1);
+    double2 w01 = make_double2(0.0, 0.0), w23 = make_double2(0.0, 0.0);
+    if (live) {
+        ci[0] = __ldg(a.cells + 3 * i);
+        ci[1] = __ldg(a.cells + 3 * i + 1);
+        ci[2] = __ldg(a.cells + 3 * i + 2);
+        if (!a.identity && a.slots == 4) {
+            jj = __ldg(reinterpret_cast<const int4 *>(a.jidx) + i);
+            w01 = __ldg(reinterpret_cast<const double2 *>(a.w) + 2 * i);
+            w23 = __ldg(reinterpret_cast<const double2 *>(a.w) + 2 * i + 1);
+        }
+    }
+    if (!a.identity)
+        for (int t = threadIdx.x; t < a.n_joints * 12; t += blockDim.x) s_aff[t] = a.aff[t];
+    __syncthreads();
     bool ok = false;
     int64_t g[3] = {0, 0, 0};
     if (live) {
-        const int32_t ci[3] = {a.cells[3 * i], a.cells[3 * i + 1], a.cells[3 * i + 2]};
         if (a.identity) {
             ok = true;
             for (int k = 0; k < 3; ++k) g[k] = ci[k];
@@ -92,9 +106,6 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
                 }
             };
             if (a.slots == 4) {
-                int4 jj = reinterpret_cast<const int4 *>(a.jidx)[i];
-                double2 w01 = reinterpret_cast<const double2 *>(a.w)[2 * i];
-                double2 w23 = reinterpret_cast<const double2 *>(a.w)[2 * i + 1];
                 slot(0, jj.x, w01.x);
                 slot(1, jj.y, w01.y);
                 slot(2, jj.z, w23.x);
