@@ -67,6 +67,24 @@ inline bool pdl_enabled() {
     return on == 1;
 }
 
+// Launch priority of the launches made through launch_pdl on this host
+// thread (0 = the stream's own); PriorityScope raises it for one launch.
+inline int &launch_priority() {
+    static thread_local int p = 0;
+    return p;
+}
+struct PriorityScope {
+    int saved;
+    explicit PriorityScope(bool on) : saved(launch_priority()) {
+        if (on) {
+            int least = 0, greatest = 0;
+            cudaDeviceGetStreamPriorityRange(&least, &greatest);
+            launch_priority() = greatest;
+        }
+    }
+    ~PriorityScope() { launch_priority() = saved; }
+};
+
 template <typename... KArgs, typename... Args>
 int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                Args... args) {
@@ -75,11 +93,20 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (launch_priority() != 0) {  // set around a launch by PriorityScope
+        at[na].id = cudaLaunchAttributePriority;
+        at[na].val.priority = launch_priority();
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
     if (e != cudaSuccess) {
         set_cuda_error(e);

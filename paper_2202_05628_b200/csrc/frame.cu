@@ -44,8 +44,9 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
                      uint32_t *live_codes, unsigned long long *wmax,
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches);
 int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st);
-int counting_finish(const int32_t *n_live, unsigned long long *wmax, uint32_t *winners,
-                    cudaStream_t st);
+int counting_finish(const int32_t *n_live, int64_t n_cap, unsigned long long *wmax,
+                    uint32_t *winners, const uint32_t *codes, uint4 *leaves, const double *sigma,
+                    const int32_t *rot_index, cudaStream_t st);
 int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
                   const artemis_camera *cam_dev, int width, int height, int sharded,
                   double lambda_th, double sigma_dep, int early_stop, int maps64, float *F,
@@ -103,6 +104,7 @@ struct artemis_frame_s {
     // masks + brick bitmap (both kept zero between frames), per-word counts,
     // per-live-cell density keys
     int counting = 0;
+    int karras_tail = 0;  // counting: Karras tree arrays built beside the render (ARTEMIS_KARRAS_TAIL)
     uint32_t *bmask = nullptr, *bocc = nullptr, *wtmp = nullptr;
     int64_t n_words = 0;
     // per live slot: 128-bit max of (density key, ~index), kept reset between frames
@@ -152,7 +154,7 @@ struct artemis_frame_s {
     // second stream of the frame (output clearing, brick map) and its
     // fork / mid / join events
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join = nullptr, ev_tail = nullptr;
     // tile-sharded frames written straight into another rank's full-frame
     // F / alpha / depth (peer memory over NVLink): artemis_frame_set_output_peer
     void *peer_out[3] = {nullptr, nullptr, nullptr};
@@ -219,6 +221,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     const artemis_asset &as = f->asset;
     int rc;
     int launches = 0;
+    bool tail_join = false;  // the Karras build runs beside the render (karras_tail)
     const bool prof = f->profile && !(flags & 2);
     NvtxStages nvtx;
     auto mark = [&](int k) {
@@ -279,18 +282,45 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                               f->wkey, f->counters + 1, f->bmeta, st, &launches);
         if (rc) return rc;
         mark(2);
-        rc = counting_finish(f->counters + 1, f->wkey, f->winners, st);
-        if (rc) return rc;
-        mark(3);
-        rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
-                                         f->n, f->left, f->right, f->bmin, f->bsize, nullptr,
-                                         f->leaves, f->winners, as.sigma, f->rot_joint, nullptr,
-                                         st);
-        if (rc) return rc;
+        if (f->karras_tail) {
+            // the leaf records come out of the finish pass, so the render
+            // needs nothing from the Karras build: the tree arrays (the
+            // rebuild stage's reference-layout output, volume.build_octree)
+            // are built on the side stream after the output clears, launched
+            // behind the render (which carries the higher launch priority) --
+            // their blocks fill the SMs the render's tail releases; the frame
+            // joins them after the render
+            rc = counting_finish(f->counters + 1, f->n, f->wkey, f->winners,
+                                 (const uint32_t *)f->live_codes, f->leaves, as.sigma,
+                                 f->rot_joint, st);
+            if (rc) return rc;
+            mark(3);
+            ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));  // the clears
+            ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
+            ARTEMIS_TRY(cudaEventRecord(f->ev_mid, st));
+            ARTEMIS_TRY(cudaStreamWaitEvent(f->side, f->ev_mid, 0));
+            rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
+                                             f->n, f->left, f->right, f->bmin, f->bsize, nullptr,
+                                             nullptr, nullptr, nullptr, nullptr, nullptr,
+                                             f->side);
+            if (rc) return rc;
+            ARTEMIS_TRY(cudaEventRecord(f->ev_tail, f->side));
+            tail_join = true;
+        } else {
+            rc = counting_finish(f->counters + 1, f->n, f->wkey, f->winners, nullptr, nullptr, nullptr,
+                                 nullptr, st);
+            if (rc) return rc;
+            mark(3);
+            rc = launch_build_tree<uint32_t>((const uint32_t *)f->live_codes, 0, f->counters + 1,
+                                             f->n, f->left, f->right, f->bmin, f->bsize, nullptr,
+                                             f->leaves, f->winners, as.sigma, f->rot_joint,
+                                             nullptr, st);
+            if (rc) return rc;
+            // the side stream only cleared the outputs: join it before the render
+            ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));
+            ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
+        }
         launches += 2;  // finish, the Karras build (count/scan/emit/slot counted above)
-        // the side stream only cleared the outputs: join it before the render
-        ARTEMIS_TRY(cudaEventRecord(f->ev_join, f->side));
-        ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_join, 0));
     } else {
     // the Karras tree arrays (reference layout) are rebuilt every frame: they
     // are the rebuild stage's output (volume.build_octree) even though the
@@ -341,6 +371,8 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     artemis_tree_view tv{f->nodes, f->leaves, 0, f->counters + 1, (double)as.resolution, &f->bmap};
     artemis_shading sh{as.coef, as.sigma, f->rot_joint, f->params->rot_inv, as.degree,
                        as.channels, 0};
+    // ahead of the Karras build on the side stream, if it runs there
+    PriorityScope prio(tail_join && !getenv("ARTEMIS_NO_RENDER_PRIO"));
     // big FLUT: views rendered together thrash L2 (configs[4] stereo, unaligned:
     // 8.86 vs 8.27 ms) -- except a stereo pair aligned by disparity (8.14 ms)
     if (vo.n > 2 && !f->small_flut) {
@@ -362,6 +394,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                            &f->params->order_on, sharded ? f->peer_out : nullptr, vo.n, vo.F, vo.A,
                            vo.D, f->n, 1, f->fast_div, f->params->view_shift, st);
     }
+    if (tail_join) ARTEMIS_TRY(cudaStreamWaitEvent(st, f->ev_tail, 0));
     mark(5);
     launches += 1;
     f->launches = launches;
@@ -535,6 +568,7 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_mid, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_join, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_tail, cudaEventDisableTiming);
         if (e != cudaSuccess) {
             set_cuda_error(e);
             rc = ARTEMIS_ERR_CUDA;
@@ -556,6 +590,8 @@ extern "C" int artemis_frame_create(const artemis_asset *a, artemis_frame *out) 
         // selects the onesweep sort + resolve path instead (A/B, tests)
         const char *env = getenv("ARTEMIS_COUNTING");
         f->counting = f->key_bytes == 4 && a->resolution <= 1024 && !(env && env[0] == '0');
+        const char *kt = getenv("ARTEMIS_KARRAS_TAIL");
+        f->karras_tail = f->counting && !(kt && kt[0] == '0');
     }
     if (!rc && f->counting) {
         const int64_t bricks = (int64_t)f->bdims[0] * f->bdims[1] * f->bdims[2];
@@ -612,7 +648,7 @@ extern "C" int artemis_frame_destroy(artemis_frame f) {
     if (f->staging) cudaFreeHost(f->staging);
     for (auto &o : f->orders)
         if (o.dev) cudaFree(o.dev);
-    for (cudaEvent_t e : {f->ev_fork, f->ev_mid, f->ev_join})
+    for (cudaEvent_t e : {f->ev_fork, f->ev_mid, f->ev_join, f->ev_tail})
         if (e) cudaEventDestroy(e);
     if (f->side) cudaStreamDestroy(f->side);
 

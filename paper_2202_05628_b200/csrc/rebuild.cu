@@ -313,22 +313,42 @@ __global__ void emit_kernel(const uint32_t *__restrict__ bocc, uint32_t *__restr
 // the winners out of the 128-bit max scratch (low word = 2^32 - 1 - index)
 // into the frame's winner array, and the scratch slots the frame used reset
 // for the next frame (a zero entry loses to every voxel)
+// With `leaves`, also the renderer's leaf records (cell, FLUT row, density,
+// rotation joint: the record build_tree32_kernel writes), so the render
+// depends on this pass only and the Karras tree arrays can be built beside it.
 __global__ void finish_kernel(const int32_t *__restrict__ n_live, ulonglong2 *__restrict__ wmax,
-                              uint32_t *__restrict__ winners) {
+                              uint32_t *__restrict__ winners, const uint32_t *__restrict__ codes,
+                              uint4 *__restrict__ leaves, const double *__restrict__ sigma,
+                              const int32_t *__restrict__ rot_index) {
     griddep_wait();
     griddep_launch_dependents();
     const int64_t n = *n_live;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        winners[i] = 0xFFFFFFFFu - (uint32_t)wmax[i].x;
+        const uint32_t row = 0xFFFFFFFFu - (uint32_t)wmax[i].x;
+        winners[i] = row;
         wmax[i] = make_ulonglong2(0ull, 0ull);
+        if (leaves) {
+            const uint32_t c = codes[i];
+            const unsigned long long sb =
+                (unsigned long long)__double_as_longlong(sigma ? __ldg(sigma + row) : 0.0);
+            leaves[2 * i] = make_uint4((uint32_t)compact_bits3(c), (uint32_t)compact_bits3(c >> 1),
+                                       (uint32_t)compact_bits3(c >> 2), row);
+            leaves[2 * i + 1] = make_uint4((uint32_t)sb, (uint32_t)(sb >> 32),
+                                           rot_index ? (uint32_t)__ldg(rot_index + row) : 0u, 0u);
+        }
     }
 }
 
-int counting_finish(const int32_t *n_live, unsigned long long *wmax, uint32_t *winners,
-                    cudaStream_t st) {
-    return launch_pdl(finish_kernel, num_sms() * 4, 256, 0, st, n_live,
-                      reinterpret_cast<ulonglong2 *>(wmax), winners);
+int counting_finish(const int32_t *n_live, int64_t n_cap, unsigned long long *wmax,
+                    uint32_t *winners, const uint32_t *codes, uint4 *leaves, const double *sigma,
+                    const int32_t *rot_index, cudaStream_t st) {
+    // leaf records: one thread per possible leaf (more loads in flight than a
+    // grid-stride loop over 4 blocks per SM)
+    const int blocks = leaves ? (int)ceil_div<int64_t>(n_cap, 256) : num_sms() * 4;
+    return launch_pdl(finish_kernel, blocks, 256, 0, st, n_live,
+                      reinterpret_cast<ulonglong2 *>(wmax), winners, codes, leaves, sigma,
+                      rot_index);
 }
 
 // live-cell rank of an in-bounds voxel's key (from its brick record)

@@ -148,8 +148,15 @@ __global__ void __launch_bounds__(kWarpThreads) lbs_warp_kernel(WarpArgs a) {
         }
     }
     if (kPipeline) {
+        // in-bounds count: one global atomic per block (a per-warp atomic on the
+        // one counter serialises ~30k same-address atomics per frame in L2)
+        __shared__ int s_in;
+        if (threadIdx.x == 0) s_in = 0;
+        __syncthreads();
         unsigned b = __ballot_sync(0xffffffffu, live && ok);
-        if ((threadIdx.x & 31) == 0 && b) atomicAdd(a.n_in, __popc(b));
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_in, __popc(b));
+        __syncthreads();
+        if (threadIdx.x == 0 && s_in) atomicAdd(a.n_in, s_in);
         if (sizeof(K) == 4 && a.bmask) {
             // mark the cell in its brick mask (word = key >> 5: at most 32
             // cells, so per-lane atomics barely contend) and the brick in the
