@@ -539,6 +539,24 @@ int artemis_host_checksum(const void *data /* host */, size_t bytes, int threads
  * race/determinism tests vary it to change the ray-to-warp schedule. */
 int artemis_debug_set_render_blocks(int max_blocks);
 
+/* artemis_host_pose_tables (host, synchronous): forward kinematics of a
+ * wrapped pose and the per-joint delta tables the warp kernel and the
+ * renderer need -- replaces the numpy body of rigging.py:228-247
+ * (forward_kinematics) and :343-347 (posed * canonical^-1 per joint), with
+ * the same doubles (the reference's numpy operation order, including the
+ * FMA chains of the ddot / dgemv kernels numpy dispatches its norm and
+ * 3x3 @ 3 products to). parents (J) parents-first, -1 = root; bind_q (J,4)
+ * bind_t (J,3) the bind locals; euler (J,3) wrapped XYZ Euler angles;
+ * global_q (4) global_t (3) the pose's global transform; canon_q (J,4)
+ * canon_t (J,3) the canonical (zero-pose) globals. Out: delta_mats (J,4,4),
+ * delta_quats (J,4), rot_inv (J,3,3). ARTEMIS_ERR_ARG for J outside
+ * [1, 256], a parent out of order or a zero quaternion on the way. */
+int artemis_host_pose_tables(int n_joints, const int32_t *parents, const double *bind_q,
+                             const double *bind_t, const double *euler, const double *global_q,
+                             const double *global_t, const double *canon_q,
+                             const double *canon_t, double *delta_mats, double *delta_quats,
+                             double *rot_inv);
+
 /* artemis_host_widen_f32 (host, synchronous): dst[r][c] = (double)src[r][c]
  * for a rows x cols block (row pitches in elements) on up to `threads` host
  * threads -- the fp32 -> fp64 step of the per-frame API's FrameBuffers

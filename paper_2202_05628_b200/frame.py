@@ -45,6 +45,7 @@ class FramePipeline:
         self.cell = (self.hi - self.lo) / self.resolution
         self.rig = rig
         self._canon = KM.canonical_globals(rig) if rig is not None else None
+        self._native_fk = None  # KM.NativePoseTables once checked against numpy
 
         def dev(a, dt):
             if isinstance(a, torch.Tensor):
@@ -110,7 +111,13 @@ class FramePipeline:
 
     # -- per frame --------------------------------------------------------------
     def tables(self, pose) -> KM.PoseTables:
-        return KM.pose_tables(self.rig, KM.PoseSpec.from_any(pose), canonical=self._canon)
+        pose = KM.PoseSpec.from_any(pose)
+        if self._native_fk is None:
+            self._native_fk = (KM.NativePoseTables(self.rig, self._canon)
+                               if KM.NativePoseTables.agrees() else False)
+        if self._native_fk:
+            return self._native_fk(pose)
+        return KM.pose_tables(self.rig, pose, canonical=self._canon)
 
     def camera(self, cam) -> _lib.Camera:
         cam = KM.PinholeCamera.from_any(cam)

@@ -270,6 +270,72 @@ def pose_tables(rig: Rig, pose: PoseSpec, canonical=None) -> PoseTables:
     )
 
 
+class NativePoseTables:
+    """pose_tables() through the native restatement (artemis_host_pose_tables,
+    csrc/hostfk.cu): the same doubles in microseconds instead of ~1.4 ms of
+    tiny numpy calls per 24-joint pose. Used only where agrees() holds -- a
+    once-per-process bit-for-bit comparison with the numpy restatement above
+    on seeded random rigs and poses (the two BLAS reductions numpy dispatches
+    to are the part that could differ between hosts)."""
+
+    _agree: bool | None = None
+
+    def __init__(self, rig: Rig, canonical=None):
+        self.rig = rig
+        canon = canonical if canonical is not None else canonical_globals(rig)
+        self.parents = np.ascontiguousarray(rig.parents, dtype=np.int32)
+        self.bind_q = np.ascontiguousarray(rig.bind_q, dtype=_F64)
+        self.bind_t = np.ascontiguousarray(rig.bind_t, dtype=_F64)
+        self.canon_q = np.ascontiguousarray(np.stack([c[0] for c in canon]), dtype=_F64)
+        self.canon_t = np.ascontiguousarray(np.stack([c[1] for c in canon]), dtype=_F64)
+
+    def __call__(self, pose: PoseSpec) -> PoseTables:
+        from . import _lib
+
+        J = self.rig.n_joints
+        euler = np.ascontiguousarray(pose.joint_rotations, dtype=_F64)
+        if euler.shape != (J, 3):
+            raise ContractViolation(f"pose has {euler.shape[0]} joints, skeleton has {J}")
+        gq = np.ascontiguousarray(pose.global_rotation, dtype=_F64)
+        gt = np.ascontiguousarray(pose.global_translation, dtype=_F64)
+        dm = np.empty((J, 4, 4))
+        dq = np.empty((J, 4))
+        ri = np.empty((J, 3, 3))
+        P = lambda a: a.ctypes.data  # noqa: E731
+        rc = _lib.load_library().artemis_host_pose_tables(J, P(self.parents), P(self.bind_q),
+                                                   P(self.bind_t), P(euler), P(gq), P(gt),
+                                                   P(self.canon_q), P(self.canon_t), P(dm), P(dq),
+                                                   P(ri))
+        if rc != 0:
+            raise ContractViolation("zero quaternion or invalid rig in forward kinematics")
+        return PoseTables(delta_mats=dm, delta_quats=dq, rot_inv=ri)
+
+    @classmethod
+    def agrees(cls) -> bool:
+        if cls._agree is None:
+            rng = np.random.default_rng(20220211)
+            ok = True
+            for trial in range(8):
+                J = 24
+                parents = np.array([-1] + [int(rng.integers(0, j)) for j in range(1, J)], np.int32)
+                bq = rng.standard_normal((J, 4))
+                bq /= np.linalg.norm(bq, axis=1, keepdims=True)
+                rig = Rig(parents=parents, bind_q=bq, bind_t=rng.standard_normal((J, 3)) * 0.3)
+                canon = canonical_globals(rig)
+                native = cls(rig, canon)
+                for _ in range(4):
+                    g = rng.standard_normal(4)
+                    pose = PoseSpec.make(rng.uniform(-4, 4, (J, 3)), g / np.linalg.norm(g),
+                                         rng.standard_normal(3))
+                    a = pose_tables(rig, pose, canonical=canon)
+                    b = native(pose)
+                    ok &= all(x.tobytes() == y.tobytes() for x, y in
+                              ((a.delta_mats, b.delta_mats), (a.delta_quats, b.delta_quats),
+                               (a.rot_inv, b.rot_inv)))
+            cls._agree = bool(ok)
+        return cls._agree
+
+
 def identity_tables() -> PoseTables:
     """The no-warp case (identity_warp, rigging.py:400-416)."""
     return PoseTables(
