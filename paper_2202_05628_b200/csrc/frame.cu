@@ -43,7 +43,8 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
                      BrickRec *recs, int32_t *table, const int dims[3], int32_t *aabb,
                      uint32_t *live_codes, unsigned long long *wmax,
                      int32_t *n_live, int32_t *n_recs, cudaStream_t st, int *launches);
-int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st);
+int counting_prepare(int32_t *counters, int n_counters, int32_t *table, const int dims[3],
+                     int32_t *aabb, cudaStream_t st);
 int counting_finish(const int32_t *n_live, int64_t n_cap, unsigned long long *wmax,
                     uint32_t *winners, const uint32_t *codes, uint4 *leaves, const double *sigma,
                     const int32_t *rot_index, cudaStream_t st);
@@ -245,8 +246,9 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         f->launches = 1;
         return rc;
     }
-    // counters: [0] in-bounds, [1] live leaves, [2..3] render ray queue (u64)
-    ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 4 * sizeof(int32_t), st));
+    // counters: [0] in-bounds, [1] live leaves, [2..3] render ray queue (u64);
+    // reset with the brick table and AABB in one kernel (counting) below
+    if (!f->counting) ARTEMIS_TRY(cudaMemsetAsync(f->counters, 0, 4 * sizeof(int32_t), st));
     // side stream: the outputs are cleared while the rebuild runs, and the
     // brick map is built beside the Karras tree (both only read the live
     // codes); joined before the render
@@ -263,7 +265,7 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
         }
     }
     if (f->counting) {
-        rc = counting_prepare(f->btable, f->bdims, f->bmeta + 1, st);
+        rc = counting_prepare(f->counters, 4, f->btable, f->bdims, f->bmeta + 1, st);
         if (rc) return rc;
     }
     rc = warp_pipeline(as.cells, f->n, as.slots, as.joint_idx, as.weights, f->params->aff,

@@ -425,14 +425,31 @@ int counting_rebuild(const uint32_t *keys, int64_t n, uint32_t sentinel, const d
     return rc;
 }
 
-// Before the warp kernel (so the kernel chain after it has no memset nodes
-// between its launches): the dense brick table and the leaf AABB reset.
-int counting_prepare(int32_t *table, const int dims[3], int32_t *aabb, cudaStream_t st) {
-    const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
-    ARTEMIS_TRY(cudaMemsetAsync(table, 0xFF, cells * sizeof(int32_t), st));
-    ARTEMIS_TRY(cudaMemsetAsync(aabb, 0x7F, 3 * sizeof(int32_t), st));
-    ARTEMIS_TRY(cudaMemsetAsync(aabb + 3, 0x80, 3 * sizeof(int32_t), st));
-    return ARTEMIS_OK;
+// Frame start, one kernel instead of four memset nodes (a graph ran them one
+// after another, behind the side stream's output clear): the frame counters
+// zeroed, the dense brick table to -1 and the leaf AABB to (+max, -max).
+__global__ void frame_prepare_kernel(int32_t *__restrict__ counters, int n_counters,
+                                     int4 *__restrict__ table4, int64_t n4,
+                                     int32_t *__restrict__ aabb) {
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i0 < n_counters) counters[i0] = 0;
+    if (aabb && i0 < 6) aabb[i0] = i0 < 3 ? 0x7F7F7F7F : (int32_t)0x80808080;
+    for (int64_t i = i0; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+        table4[i] = make_int4(-1, -1, -1, -1);
+}
+
+int counting_prepare(int32_t *counters, int n_counters, int32_t *table, const int dims[3],
+                     int32_t *aabb, cudaStream_t st) {
+    const size_t cells = table ? (size_t)dims[0] * dims[1] * dims[2] : 0;
+    if (cells % 4) {  // not a whole number of int4 (never for 8^3-brick grids)
+        ARTEMIS_TRY(cudaMemsetAsync(table, 0xFF, cells * sizeof(int32_t), st));
+    }
+    const int64_t n4 = cells % 4 ? 0 : (int64_t)(cells / 4);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div<int64_t>(n4, 256),
+                                                                   num_sms() * 4));
+    frame_prepare_kernel<<<blocks, 256, 0, st>>>(counters, n_counters,
+                                                  reinterpret_cast<int4 *>(table), n4, aabb);
+    return ARTEMIS_LAUNCHED();
 }
 
 }  // namespace artemis
