@@ -399,12 +399,35 @@ class FramePipeline:
         for bb in pending:
             yield expand(bb)
 
+    def twin(self) -> "FramePipeline":
+        """A second pipeline over the SAME device asset arrays (no upload) with
+        its own frame state, stream and graphs: run_stream alternates frames
+        between the two, so frame k+1's warp and rebuild start on the SMs
+        frame k's render tail releases instead of after the whole render."""
+        if getattr(self, "_twin", None) is None:
+            self._twin = FramePipeline(self.d_cells, self.d_jidx, self.d_w, None, self.degree,
+                                       self.channels, self.resolution, self.lo, self.hi,
+                                       rig=self.rig, max_joints=int(self._asset.max_joints),
+                                       device_flut=(self.coef, self.sigma))
+        return self._twin
+
     def _run_stream_box(self, items, *, lambda_th, sigma_dep, early_stop):
         L = _lib.lib()
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream()
             self._stream_bufs = {}
         cs = self._copy_stream
+        # frames alternate between this pipeline and its twin (buffer b is
+        # always rendered by pipeline b) while the FLUT fits in half the L2:
+        # then two frames in flight share it and frame k+1's rebuild fills
+        # frame k's render tail (configs[0] stream 0.295 -> 0.209 ms/frame);
+        # with a FLUT beyond L2 two renders in flight evict each other's rows
+        # (configs[2] 1.54 -> 1.74 ms/frame), so one pipeline.
+        # ARTEMIS_STREAM_TWIN=0/1 forces either.
+        env = os.environ.get("ARTEMIS_STREAM_TWIN", "")
+        l2 = getattr(torch.cuda.get_device_properties(self.coef.device), "L2_cache_size", 126 << 20)
+        small = self.coef.numel() * self.coef.element_size() <= 0.5 * l2
+        pipes = [self, self.twin()] if (env == "1" or (env != "0" and small)) else [self, self]
         C_ = self.channels
         self.last_stream_d2h_bytes = []
 
@@ -448,14 +471,15 @@ class FramePipeline:
         for k, (pose, camera) in enumerate(items):
             cam = camera if isinstance(camera, _lib.Camera) else self.camera(camera)
             bb = bufs(cam.width, cam.height, k % 2)
-            self.stream.wait_event(bb["copied"])  # its device maps have been read out
-            F, A, D = self.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
-                               early_stop=early_stop, out=bb["dev"])
+            pp = pipes[k % 2]
+            pp.stream.wait_event(bb["copied"])  # its device maps have been read out
+            F, A, D = pp.run(pose, cam, lambda_th=lambda_th, sigma_dep=sigma_dep,
+                             early_stop=early_stop, out=bb["dev"])
             check(L.artemis_frame_bbox(ptr(A), ptr(D), 0, cam.width, cam.height, ptr(bb["dbox"]),
-                                       self.stream.cuda_stream or None), "frame_bbox")
-            with torch.cuda.stream(self.stream):
+                                       pp.stream.cuda_stream or None), "frame_bbox")
+            with torch.cuda.stream(pp.stream):
                 bb["hbox"].copy_(bb["dbox"], non_blocking=True)
-            bb["boxed"].record(self.stream)
+            bb["boxed"].record(pp.stream)
             pending.append(bb)
             if len(pending) >= 2:
                 launch_copy(pending[-2])
@@ -574,6 +598,9 @@ class FramePipeline:
                                                       o.ctypes.data), "frame_set_tile_order")
 
     def close(self):
+        if getattr(self, "_twin", None) is not None:
+            self._twin.close()
+            self._twin = None
         if getattr(self, "_h", None):
             _lib.lib().artemis_frame_destroy(self._h)
             self._h = None
