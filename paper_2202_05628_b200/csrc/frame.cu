@@ -252,30 +252,17 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
     // side stream: the outputs are cleared while the rebuild runs, and the
     // brick map is built beside the Karras tree (both only read the live
     // codes); joined before the render
-    // The clear (a memset kernel over the whole F map: ~23 us of the whole
-    // machine at configs[2]) is forked after the warp kernel: forked first,
-    // it held the warp kernel back until it was done (kernel timeline,
-    // scripts/timeline.py); after the warp it shares the GPU with the small
-    // count/scan/emit passes instead. ARTEMIS_CLEAR_FIRST=1: forked first.
-    static const bool clear_first = getenv("ARTEMIS_CLEAR_FIRST") &&
-                                    getenv("ARTEMIS_CLEAR_FIRST")[0] == '1';
-    auto fork_clears = [&]() -> int {
-        ARTEMIS_TRY(cudaEventRecord(f->ev_fork, st));
-        ARTEMIS_TRY(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    ARTEMIS_TRY(cudaEventRecord(f->ev_fork, st));
+    ARTEMIS_TRY(cudaStreamWaitEvent(f->side, f->ev_fork, 0));
+    {
         const int64_t px = (int64_t)width * height;
         const bool peer = sharded && f->peer_out[0];
         for (int v = 0; v < vo.n && !peer; ++v) {
-            const int r = render_clear_outputs(vo.n > 1 ? vo.F[v] : F, vo.n > 1 ? vo.A[v] : A,
-                                               vo.n > 1 ? vo.D[v] : D, px, as.channels,
-                                               vo.n > 1 ? 0 : sharded, (flags & 8) ? 1 : 0,
-                                               f->side);
-            if (r) return r;
+            rc = render_clear_outputs(vo.n > 1 ? vo.F[v] : F, vo.n > 1 ? vo.A[v] : A,
+                                      vo.n > 1 ? vo.D[v] : D, px, as.channels,
+                                      vo.n > 1 ? 0 : sharded, (flags & 8) ? 1 : 0, f->side);
+            if (rc) return rc;
         }
-        return ARTEMIS_OK;
-    };
-    if (clear_first || !f->counting) {
-        rc = fork_clears();
-        if (rc) return rc;
     }
     if (f->counting) {
         rc = counting_prepare(f->counters, 4, f->btable, f->bdims, f->bmeta + 1, st);
@@ -287,10 +274,6 @@ int enqueue_frame(artemis_frame f, int identity, int n_joints, int width, int he
                        f->keys, f->vals, f->rot_joint, f->counters, f->sentinel, identity,
                        f->counting ? f->bmask : nullptr, f->counting ? f->bocc : nullptr, st);
     if (rc) return rc;
-    if (f->counting && !clear_first) {
-        rc = fork_clears();
-        if (rc) return rc;
-    }
     launches += 1;
     mark(1);
     if (f->counting) {
