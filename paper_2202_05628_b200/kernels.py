@@ -290,6 +290,11 @@ def set_cache_policy(policy: str) -> None:
     invalidate_cache()
 
 
+def cache_policy() -> str:
+    """The current cache policy ("content" or "identity")."""
+    return _POLICY
+
+
 def invalidate_cache() -> None:
     """Drop every cached device FLUT / tree (after in-place edits under the
     "identity" policy; harmless otherwise)."""

@@ -32,6 +32,7 @@ pointer, shape or a strided content sample).
 from __future__ import annotations
 
 import collections
+import threading
 import time
 import weakref
 
@@ -357,11 +358,21 @@ class _DeviceAssets:
         self.capacity = capacity
         self._d: collections.OrderedDict = collections.OrderedDict()
 
-    def get(self, asset):
+    def resident(self, asset):
+        """(pipeline, signature) cached for this very asset object, without
+        digesting its arrays (the caller checks the signature itself), or
+        None."""
+        ent = self._d.get(id(asset))
+        if ent is None or ent[0]() is not asset:
+            return None
+        return ent[2], ent[1]
+
+    def get(self, asset, sig=None):
         if not _frame_eligible(asset):
             return None
         key = id(asset)
-        sig = _asset_sig(asset)
+        if sig is None:
+            sig = _asset_sig(asset)
         ent = self._d.get(key)
         if ent is not None:
             ref, esig, fp = ent
@@ -408,10 +419,52 @@ DEVICE_ASSETS = _DeviceAssets()
 
 
 def _frame_device(asset, pose, camera, opts, timed: bool):
-    """One frame through the resident FramePipeline; (FrameBuffers, times)."""
+    """One frame through the resident FramePipeline; (FrameBuffers, times).
+
+    Under the "content" cache policy the asset's arrays are digested on every
+    call (an in-place edit must take effect, as in the reference, which
+    re-reads them per frame). When this asset object already has a resident
+    pipeline, the digest runs on a host thread WHILE that pipeline renders
+    the frame and reads it out; the frame is returned only if the digest
+    equals the resident one, otherwise the pipeline is rebuilt from the new
+    content and the frame rendered again -- the result is always that of
+    the current content, and the digest's host time overlaps the frame."""
+    if K.cache_policy() == "content" and _frame_eligible(asset):
+        res = DEVICE_ASSETS.resident(asset)
+        if res is not None:
+            fp, esig = res
+            box = {}
+
+            def digest():
+                try:
+                    box["sig"] = _asset_sig(asset)
+                except BaseException as e:  # re-raised on the calling thread
+                    box["err"] = e
+
+            th = threading.Thread(target=digest, name="artemis-asset-digest")
+            th.start()
+            out = err = None
+            try:
+                out = _frame_on(fp, asset, pose, camera, opts, timed)
+            except Exception as e:  # stale content may be the cause: decided below
+                err = e
+            finally:
+                th.join()
+            if "err" in box:
+                raise box["err"]
+            if box["sig"] == esig:
+                if err is not None:
+                    raise err
+                return out
+            fp = DEVICE_ASSETS.get(asset, sig=box["sig"])
+            return None if fp is None else _frame_on(fp, asset, pose, camera, opts, timed)
     fp = DEVICE_ASSETS.get(asset)
     if fp is None:
         return None
+    return _frame_on(fp, asset, pose, camera, opts, timed)
+
+
+def _frame_on(fp, asset, pose, camera, opts, timed: bool):
     rigged = getattr(asset, "skeleton", None) is not None
     if pose is not None and not rigged and not _is_canonical(pose):
         raise ContractViolation("asset has no rig; only the canonical pose renders")

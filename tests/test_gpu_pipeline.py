@@ -462,6 +462,23 @@ class TestResidentFrames:
         fb2 = P.render_frame(asset, pose, cam)
         assert P.DEVICE_ASSETS.get(asset) is not fp
         assert not np.array_equal(fb.alpha, fb2.alpha)
+        # in-place edits (same array object) are seen by the digest that runs
+        # beside the resident pipeline's frame: the frame is rendered again
+        fp2 = P.DEVICE_ASSETS.get(asset)
+        for timed in (False, True):
+            asset.flut.data[:, 0] += 0.25  # the reference's SparseAdam.step edits in place
+            call = P.timed_render_frame if timed else P.render_frame
+            got = call(asset, pose, cam)
+            got = got[0] if timed else got
+            assert P.DEVICE_ASSETS.get(asset) is not fp2
+            fp2 = P.DEVICE_ASSETS.get(asset)
+            want = P._timed_render_frame_api(asset, pose, cam)[0]
+            assert np.array_equal(got.features, want.features)
+            assert np.array_equal(got.alpha, want.alpha)
+            assert np.array_equal(got.depth, want.depth)
+        again = P.render_frame(asset, pose, cam)  # unchanged: the resident frame stands
+        assert P.DEVICE_ASSETS.get(asset) is fp2
+        assert np.array_equal(again.features, want.features)
         still = Asset(mini, rigged=False)
         fb3 = P.render_frame(still, None, cam)
         want = P._timed_render_frame_api(still, None, cam)[0]
