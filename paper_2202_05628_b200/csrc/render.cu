@@ -94,6 +94,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_FLAT_SHADE
 #define ARTEMIS_FLAT_SHADE 0  // 1: shade a flat member list per level (see phase C)
 #endif
+#ifndef ARTEMIS_SORT_ITEMS
+#define ARTEMIS_SORT_ITEMS 1  // phase C: a level's row groups in passes by member count
+#endif
 #ifndef ARTEMIS_ROW_HINT
 #define ARTEMIS_ROW_HINT 0  // 1: FLUT row loads carry an L2 evict_last policy
 #endif
@@ -1033,8 +1036,33 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #ifdef ARTEMIS_PHASE_CLOCKS
                 if (lane == 0) atomicAdd(&g_shade_stats[1], (unsigned long long)cnt);
 #endif
+#if ARTEMIS_SORT_ITEMS
+                // The lane groups of one pass run their member loops in
+                // lockstep, so a pass costs its largest group: order the row
+                // groups by member count (descending, capped at 8; ties by
+                // lane) so each pass holds groups of similar size. Groups of
+                // one level belong to different rays: any order is exact.
+                int slot;
+                {
+                    const unsigned key = 8u - (unsigned)min(__popc(grpm), 8);  // 0..7
+                    unsigned same = ml;
+                    slot = 0;
+#pragma unroll
+                    for (int b = 2; b >= 0; --b) {
+                        const unsigned bb = __ballot_sync(0xffffffffu, (key >> b) & 1u);
+                        if ((key >> b) & 1u) {
+                            slot += __popc(same & ~bb);
+                            same &= bb;
+                        } else {
+                            same &= ~bb;
+                        }
+                    }
+                    slot += __popc(same & lt);
+                }
+#else
+                const int slot = __popc(ml & lt);
+#endif
                 if (leader) {
-                    const int slot = __popc(ml & lt);
                     wl[slot] = (uint16_t)lane;
                     wm[slot] = grpm;
                 }

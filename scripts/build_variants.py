@@ -52,6 +52,7 @@ VARIANTS = {
     "q5t56": ("ARTEMIS_QCAP=5", "ARTEMIS_QTHRESH=56"),
     "t64": ("ARTEMIS_QTHRESH=64",),
     "bpf": ("ARTEMIS_ROW_PREFETCH=4",),
+    "nosort": ("ARTEMIS_SORT_ITEMS=0",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
