@@ -95,7 +95,7 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #define ARTEMIS_FLAT_SHADE 0  // 1: shade a flat member list per level (see phase C)
 #endif
 #ifndef ARTEMIS_SORT_ITEMS
-#define ARTEMIS_SORT_ITEMS 1  // phase C: a level's row groups in passes by member count
+#define ARTEMIS_SORT_ITEMS 1  // phase C: row groups in passes by member count (2: also L2-resident FLUTs)
 #endif
 #ifndef ARTEMIS_ROW_HINT
 #define ARTEMIS_ROW_HINT 0  // 1: FLUT row loads carry an L2 evict_last policy
@@ -1042,8 +1042,11 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 // groups by member count (descending, capped at 8; ties by
                 // lane) so each pass holds groups of similar size. Groups of
                 // one level belong to different rays: any order is exact.
-                int slot;
-                {
+                // Only when the FLUT is not L2-resident (the passes wait on
+                // L2 misses; with an L2-resident FLUT the ranking's ballots
+                // cost more than they save: configs[1] 0.842 -> 0.854 ms).
+                int slot = __popc(ml & lt);
+                if (ARTEMIS_SORT_ITEMS == 2 || !p.no_row_prefetch) {
                     const unsigned key = 8u - (unsigned)min(__popc(grpm), 8);  // 0..7
                     unsigned same = ml;
                     slot = 0;

@@ -53,6 +53,7 @@ VARIANTS = {
     "t64": ("ARTEMIS_QTHRESH=64",),
     "bpf": ("ARTEMIS_ROW_PREFETCH=4",),
     "nosort": ("ARTEMIS_SORT_ITEMS=0",),
+    "sortall": ("ARTEMIS_SORT_ITEMS=2",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
