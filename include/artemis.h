@@ -539,6 +539,12 @@ int artemis_host_checksum(const void *data /* host */, size_t bytes, int threads
  * race/determinism tests vary it to change the ray-to-warp schedule. */
 int artemis_debug_set_render_blocks(int max_blocks);
 
+/* Test hook (no reference counterpart): force the render launches' "FLUT is
+ * L2-resident" decision (-1 = automatic by FLUT size vs L2, 0 = not resident:
+ * L2 row prefetch and the phase-C member-count ranking on, 1 = resident:
+ * both off). The maps must not depend on it. */
+int artemis_debug_set_flut_l2_resident(int mode);
+
 /* artemis_host_pose_tables (host, synchronous): forward kinematics of a
  * wrapped pose and the per-joint delta tables the warp kernel and the
  * renderer need -- replaces the numpy body of rigging.py:228-247

@@ -144,6 +144,7 @@ _SIGS = {
     "artemis_host_widen_f32": (INT, [P, I64, I64, I64, P, I64, INT]),
     "artemis_host_pose_tables": (INT, [INT, P, P, P, P, P, P, P, P, P, P, P]),
     "artemis_debug_set_render_blocks": (INT, [INT]),
+    "artemis_debug_set_flut_l2_resident": (INT, [INT]),
     "artemis_debug_division_selftest": (INT, [I64, C.c_uint64, P, P]),
 }
 

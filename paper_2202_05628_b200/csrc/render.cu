@@ -1186,6 +1186,9 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 // test hook (artemis_debug_set_render_blocks): cap the persistent render
 // grid so a test can vary the ray-to-warp schedule; results must not change
 static int g_render_block_cap = 0;
+// test hook (artemis_debug_set_flut_l2_resident): -1 automatic, 0/1 force the
+// "FLUT L2-resident" launch flag (row prefetch off, no phase-C ranking when 1)
+static int g_flut_l2_resident = -1;
 
 template <int kMode, int kRays, bool kVec, bool kDDA, bool kFast = false>
 int launch_render_vec(int degree, const RenderArgs &a, int64_t warps, cudaStream_t st) {
@@ -1328,7 +1331,9 @@ int render_camera(const artemis_tree_view *tree, const artemis_shading *shade,
         }
         const int stride = shade->coef_stride > 0 ? shade->coef_stride
                                                   : (shade->degree + 1) * (shade->degree + 1) * shade->channels;
-        a.no_row_prefetch = flut_rows > 0 && (double)flut_rows * stride * 4.0 <= 0.5 * l2;
+        a.no_row_prefetch = g_flut_l2_resident >= 0
+                                ? g_flut_l2_resident
+                                : flut_rows > 0 && (double)flut_rows * stride * 4.0 <= 0.5 * l2;
         a.n_rows = flut_rows;
     }
     if (n_views > 1) {  // several views of one tree in one launch (unsharded, own outputs)
@@ -1621,6 +1626,12 @@ extern "C" int artemis_debug_division_selftest(int64_t n, uint64_t seed,
     }
     cudaFree(d);
     return rc;
+}
+
+extern "C" int artemis_debug_set_flut_l2_resident(int mode) {
+    if (mode < -1 || mode > 1) return ARTEMIS_ERR_ARG;
+    g_flut_l2_resident = mode;
+    return ARTEMIS_OK;
 }
 
 extern "C" int artemis_debug_set_render_blocks(int max_blocks) {

@@ -125,3 +125,45 @@ def test_reciprocal_corrected_division_is_exact():
     bad = ctypes.c_ulonglong(0)
     assert L.artemis_debug_division_selftest(1 << 28, 12345, ctypes.byref(bad), None) == 0
     assert bad.value == 0
+
+
+def test_row_group_ranking_is_exact():
+    """Phase C's member-count ranking of row groups (and the L2 row
+    prefetch) run only when the FLUT is not L2-resident -- at test sizes the
+    automatic decision turns both off. Forcing each decision must give
+    bit-identical maps in camera mode, multi-view and API mode (walk + DFS):
+    the ranking only reorders groups of different rays within a level."""
+    from paper_2202_05628_b200.frame import FramePipeline
+
+    L = _lib.lib()
+    sc = S.make_scene("c1", frames=1, image=(160, 128))
+    fp = FramePipeline.from_scene(sc)
+    pose = KM.PoseSpec.make(sc.poses[0])
+    tables = KM.pose_tables(sc.rig, pose)
+    fr = oracle.render_frame(sc, tables, sc.cameras[0][0], render=False)
+    old = K.DeviceTree.MAX_BRICK_TABLE
+    outs = {}
+    try:
+        for mode in (1, 0, -1):
+            assert L.artemis_debug_set_flut_l2_resident(mode) == 0
+            cam = [x.clone() for x in fp.run(pose, sc.cameras[0][1], graph=False,
+                                             lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep)]
+            views = fp.render_views(pose, sc.cameras[0][:3], graph=False)
+            fp.stream.synchronize()
+            got = [x.cpu().numpy() for x in cam] + [x.cpu().numpy() for v in views for x in v]
+            for enum in ("walk", "dfs"):
+                K.DeviceTree.MAX_BRICK_TABLE = 0 if enum == "dfs" else old
+                K.invalidate_cache()
+                args = (*fr["tree"], fr["origins_g"], fr["dirs_g"], fr["dirs_w"], 0.0, np.inf,
+                        sc.flut32, fr["rotation_joint"], tables.rot_inv, sc.degree, sc.channels)
+                got += list(K.render_rays(*args, sc.lambda_th, sc.sigma_dep, True))
+            outs[mode] = got
+    finally:
+        assert L.artemis_debug_set_flut_l2_resident(-1) == 0
+        K.DeviceTree.MAX_BRICK_TABLE = old
+        K.invalidate_cache()
+        fp.close()
+    assert (outs[1][1] > 0).sum() > 1000
+    for mode in (0, -1):
+        for a, b in zip(outs[mode], outs[1]):
+            assert np.array_equal(a, b), mode
