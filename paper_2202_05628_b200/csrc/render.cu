@@ -94,6 +94,9 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #ifndef ARTEMIS_FLAT_SHADE
 #define ARTEMIS_FLAT_SHADE 0  // 1: shade a flat member list per level (see phase C)
 #endif
+#ifndef ARTEMIS_SPLIT_M
+#define ARTEMIS_SPLIT_M 0  // phase C: split row groups into items of <= M members (0: off)
+#endif
 #ifndef ARTEMIS_SORT_ITEMS
 #define ARTEMIS_SORT_ITEMS 1  // phase C: row groups in passes by member count (2: also L2-resident FLUTs)
 #endif
@@ -1031,7 +1034,33 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                     continue;
                 }
 #endif
+#if ARTEMIS_SPLIT_M > 0
+                // a group's members in lane order, dealt as items of <= M
+                // members: the head of each item is the lane whose rank in
+                // the group is a multiple of M; its mask is the next M members
+                unsigned imask = 0;
+                bool ihead = false;
+                if (kVec && vis) {
+                    const int r = __popc(grpm & lt);
+                    ihead = (r % ARTEMIS_SPLIT_M) == 0;
+                    unsigned m = grpm & ~lt;
+#pragma unroll
+                    for (int j = 0; j < ARTEMIS_SPLIT_M; ++j) {
+                        imask |= m & (0u - m);
+                        m &= m - 1;
+                    }
+                } else {
+                    ihead = leader;
+                    imask = grpm;
+                }
+                const unsigned ml = __ballot_sync(0xffffffffu, ihead);
+#define ARTEMIS_ITEM_MASK imask
+#define ARTEMIS_ITEM_HEAD ihead
+#else
                 const unsigned ml = __ballot_sync(0xffffffffu, leader);
+#define ARTEMIS_ITEM_MASK grpm
+#define ARTEMIS_ITEM_HEAD leader
+#endif
                 const int cnt = __popc(ml);
 #ifdef ARTEMIS_PHASE_CLOCKS
                 if (lane == 0) atomicAdd(&g_shade_stats[1], (unsigned long long)cnt);
@@ -1047,7 +1076,7 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 // cost more than they save: configs[1] 0.842 -> 0.854 ms).
                 int slot = __popc(ml & lt);
                 if (ARTEMIS_SORT_ITEMS == 2 || !p.no_row_prefetch) {
-                    const unsigned key = 8u - (unsigned)min(__popc(grpm), 8);  // 0..7
+                    const unsigned key = 8u - (unsigned)min(__popc(ARTEMIS_ITEM_MASK), 8);  // 0..7
                     unsigned same = ml;
                     slot = 0;
 #pragma unroll
@@ -1065,10 +1094,12 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 #else
                 const int slot = __popc(ml & lt);
 #endif
-                if (leader) {
+                if (ARTEMIS_ITEM_HEAD) {
                     wl[slot] = (uint16_t)lane;
-                    wm[slot] = grpm;
+                    wm[slot] = ARTEMIS_ITEM_MASK;
                 }
+#undef ARTEMIS_ITEM_MASK
+#undef ARTEMIS_ITEM_HEAD
                 __syncwarp();
                 for (int item = grp; item - grp < cnt; item += hpi) {
                     if (item >= cnt) continue;
