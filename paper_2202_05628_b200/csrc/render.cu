@@ -95,7 +95,10 @@ constexpr int kEnd = (int)0x80000000;  // empty-stack marker (never a node or ~l
 #define ARTEMIS_FLAT_SHADE 0  // 1: shade a flat member list per level (see phase C)
 #endif
 #ifndef ARTEMIS_SPLIT_M
-#define ARTEMIS_SPLIT_M 0  // phase C: split row groups into items of <= M members (0: off)
+#define ARTEMIS_SPLIT_M 2  // phase C, L2-resident FLUT: row groups as items of <= M members (0: off)
+#endif
+#ifndef ARTEMIS_SPLIT_ALL
+#define ARTEMIS_SPLIT_ALL 0  // 1: split whatever the FLUT size (experiment)
 #endif
 #ifndef ARTEMIS_SORT_ITEMS
 #define ARTEMIS_SORT_ITEMS 1  // phase C: row groups in passes by member count (2: also L2-resident FLUTs)
@@ -1035,12 +1038,18 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
                 }
 #endif
 #if ARTEMIS_SPLIT_M > 0
-                // a group's members in lane order, dealt as items of <= M
-                // members: the head of each item is the lane whose rank in
-                // the group is a multiple of M; its mask is the next M members
+                // With an L2-resident FLUT a group's members, in lane order,
+                // are dealt as items of <= M members (the head of each item is
+                // the lane whose rank in the group is a multiple of M; its mask
+                // is the next M members), so a pass no longer waits on one
+                // large group: the items of one row re-read it from L1/L2,
+                // which is cheap only when the row is L2-resident (configs[1]
+                // 0.846 -> 0.803 ms; configs[2] +1 %, configs[4] +0.6 %, where
+                // the member-count ranking below balances the passes instead).
+                // Items of one level belong to different rays: exact.
                 unsigned imask = 0;
                 bool ihead = false;
-                if (kVec && vis) {
+                if (kVec && vis && (ARTEMIS_SPLIT_ALL || p.no_row_prefetch)) {
                     const int r = __popc(grpm & lt);
                     ihead = (r % ARTEMIS_SPLIT_M) == 0;
                     unsigned m = grpm & ~lt;

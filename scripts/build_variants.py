@@ -54,9 +54,9 @@ VARIANTS = {
     "bpf": ("ARTEMIS_ROW_PREFETCH=4",),
     "nosort": ("ARTEMIS_SORT_ITEMS=0",),
     "sortall": ("ARTEMIS_SORT_ITEMS=2",),
-    "split2": ("ARTEMIS_SPLIT_M=2",),
+    "split2all": ("ARTEMIS_SPLIT_ALL=1",),
     "split3": ("ARTEMIS_SPLIT_M=3",),
-    "split4": ("ARTEMIS_SPLIT_M=4",),
+    "nosplit": ("ARTEMIS_SPLIT_M=0",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
