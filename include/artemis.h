@@ -541,8 +541,9 @@ int artemis_debug_set_render_blocks(int max_blocks);
 
 /* Test hook (no reference counterpart): force the render launches' "FLUT is
  * L2-resident" decision (-1 = automatic by FLUT size vs L2, 0 = not resident:
- * L2 row prefetch and the phase-C member-count ranking on, 1 = resident:
- * both off). The maps must not depend on it. */
+ * L2 row prefetch and the phase-C member-count ranking, 1 = resident: no
+ * prefetch, row groups split into items of <= 2 members). The maps must not
+ * depend on it. */
 int artemis_debug_set_flut_l2_resident(int mode);
 
 /* artemis_host_pose_tables (host, synchronous): forward kinematics of a

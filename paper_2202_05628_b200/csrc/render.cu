@@ -1227,7 +1227,8 @@ __global__ void __launch_bounds__(kRenderThreads, ARTEMIS_MIN_BLOCKS) render_ker
 // grid so a test can vary the ray-to-warp schedule; results must not change
 static int g_render_block_cap = 0;
 // test hook (artemis_debug_set_flut_l2_resident): -1 automatic, 0/1 force the
-// "FLUT L2-resident" launch flag (row prefetch off, no phase-C ranking when 1)
+// "FLUT L2-resident" launch flag (1: no row prefetch, phase-C groups split;
+// 0: row prefetch, phase-C member-count ranking)
 static int g_flut_l2_resident = -1;
 
 template <int kMode, int kRays, bool kVec, bool kDDA, bool kFast = false>

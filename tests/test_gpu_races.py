@@ -128,11 +128,12 @@ def test_reciprocal_corrected_division_is_exact():
 
 
 def test_row_group_ranking_is_exact():
-    """Phase C's member-count ranking of row groups (and the L2 row
-    prefetch) run only when the FLUT is not L2-resident -- at test sizes the
-    automatic decision turns both off. Forcing each decision must give
+    """Phase C balances its passes by ranking row groups by member count
+    (with the L2 row prefetch) when the FLUT is not L2-resident, and by
+    splitting groups into items of <= 2 members when it is -- at test sizes
+    the automatic decision is "resident". Forcing each decision must give
     bit-identical maps in camera mode, multi-view and API mode (walk + DFS):
-    the ranking only reorders groups of different rays within a level."""
+    both only regroup the shading of different rays within a level."""
     from paper_2202_05628_b200.frame import FramePipeline
 
     L = _lib.lib()
