@@ -124,6 +124,14 @@ class RenderOptions:
             raise ContractViolation("lambda_th must be in (0, 1)")
         if self.sigma_dep < 0.0:
             raise ContractViolation("sigma_dep must be >= 0")
+        # render.py:56-63: background flattened to fp64, image_size positive
+        if self.background is not None:
+            bg = np.asarray(self.background, dtype=np.float64).reshape(-1)
+            object.__setattr__(self, "background", bg)
+        if self.image_size is not None:
+            w, h = self.image_size
+            if w < 1 or h < 1:
+                raise ContractViolation("image_size must be positive")
 
 
 @dataclass(frozen=True)

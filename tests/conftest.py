@@ -37,6 +37,11 @@ def golden_mini():
 
 
 @pytest.fixture(scope="session")
+def golden_scaled():
+    return load_golden("scaled")
+
+
+@pytest.fixture(scope="session")
 def golden_c0():
     return load_golden("scene_c0")
 

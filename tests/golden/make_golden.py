@@ -29,6 +29,10 @@ and registered as `animvox._core`) and records, on seeded inputs:
                    and the exception class for each corrupted variant
 * fit.npz          the reference's SparseAdam steps, collision-pair term
                    (np.add.at) and L1 sign gradients on seeded inputs
+* scaled.npz       the 64^3 scene rendered through render_view with
+                   RenderOptions.image_size set (render._scaled_camera,
+                   render.py:129-143): the scaled intrinsics, ray directions
+                   and the F/A/D maps at 48x40 and 96x80
 * scene_c0.npz     configs[0] at full size (128^3, 256^2): SHA-256 digests of
                    every exact array plus a pixel subsample of the maps
 * scene_c2.npz     configs[2] at full size (512^3, 1024^2, C = 32 through a
@@ -530,8 +534,38 @@ def fit_fixtures():
                 loss=np.float64(FIT.loss_rgba(F, A, gt_f, gt_a)))
 
 
+def scaled_fixtures():
+    """render_view with opts.image_size (render.py:129-143, 322-363) on the
+    64^3 scene: the camera the reference derives and the maps it renders, at a
+    size below and a size above the camera's own 64x64 (non-square both)."""
+    sc = S.make_scene("c0", resolution=64, image=(64, 64))
+    voxels, flut, skel, weights, pose = reference_objects(sc)
+    warp = RG.warp_voxels(voxels, weights, skel, pose)
+    resolved = RG.resolve_collisions(warp, flut)
+    octree = V.build_octree(resolved.cells, resolved.flut_indices,
+                            resolution=voxels.resolution, bounds=voxels.bounds)
+    rcam = reference_camera(sc.cameras[0][0])
+    out = {"sizes": np.array([[48, 40], [96, 80]], dtype=np.int64)}
+    for i, (w, h) in enumerate(out["sizes"].tolist()):
+        cam = R._scaled_camera(rcam, (w, h))
+        out[f"intr{i}"] = np.array([cam.fx, cam.fy, cam.cx, cam.cy], dtype=np.float64)
+        out[f"wh{i}"] = np.array([cam.width, cam.height], dtype=np.int64)
+        _, dirs = G.rays_for_camera(cam)
+        out[f"sha_rays_d{i}"] = np.array(digest(dirs))
+        opts = R.RenderOptions(lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep,
+                               image_size=(w, h))
+        frame = R.render_view(octree, flut, warp, rcam, opts)
+        out[f"F{i}"] = frame.features
+        out[f"A{i}"] = frame.alpha
+        out[f"D{i}"] = frame.depth
+    return out
+
+
 def main(which):
     t = time.time()
+    if "scaled" in which:
+        np.savez_compressed(os.path.join(HERE, "scaled.npz"), **scaled_fixtures())
+        print("scaled.npz", time.time() - t)
     if "kernels" in which:
         np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernel_fixtures())
         print("kernels.npz", time.time() - t)
@@ -565,4 +599,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "asset", "fit", "c0", "c2"])
+    main(sys.argv[1:] or ["kernels", "mini", "backward", "post", "asset", "fit", "scaled", "c0", "c2"])

@@ -139,6 +139,33 @@ class TestDropIns:
         assert np.max(np.abs(fb.alpha - g["A"])) <= 1e-9
         assert digest(fb.depth) == str(g["sha_depth"])
 
+    def test_render_view_image_size(self, P, mini, golden_scaled):
+        """RenderOptions.image_size re-scales the camera (render._scaled_camera,
+        render.py:129-143, 331): maps of the reference's render_view at 48x40
+        and 96x80 from the 64x64 camera, through render_view and the resident
+        render_frame."""
+        from paper_2202_05628_b200.types import RenderOptions
+
+        g = golden_scaled
+        sc = mini
+        warp = P.warp_voxels(Vox(sc), Weights(sc), sc.rig, KM.PoseSpec.make(sc.poses[0]))
+        res = P.resolve_collisions(warp, Flut(sc))
+        oc = P.build_octree(res.cells, res.flut_indices, resolution=sc.resolution,
+                            bounds=Vox(sc).bounds)
+        P.DEVICE_ASSETS.clear()
+        asset = Asset(sc)
+        for i, (w, h) in enumerate(g["sizes"].tolist()):
+            opts = RenderOptions(lambda_th=sc.lambda_th, sigma_dep=sc.sigma_dep,
+                                 image_size=(w, h))
+            fb = P.render_view(oc, Flut(sc), warp, sc.cameras[0][0], opts)
+            fr = P.render_frame(asset, KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0], opts)
+            for got in (fb, fr):
+                assert got.alpha.shape == (h, w) and got.features.shape == (h, w, sc.channels)
+                err = np.abs(got.features - g[f"F{i}"])
+                assert err.max() <= F_MAX and err.mean() <= F_MEAN
+                assert np.max(np.abs(got.alpha - g[f"A{i}"])) <= 1e-9
+                assert np.array_equal(got.depth, g[f"D{i}"])
+
     def test_duplicate_cells_rejected(self, P):
         from paper_2202_05628_b200.errors import DuplicateMortonError
         from paper_2202_05628_b200.types import Bounds
