@@ -97,6 +97,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
                 raise RuntimeError(f"nvcc failed on {src}:\n{log}")
         tmp_lib = os.path.join(tmp, "libartemis.so")
         subprocess.run([cc, *ARCH, "-shared", "-o", tmp_lib, *objs, "-lcudart"], check=True)
+        os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
         shutil.copy2(tmp_lib, target + ".tmp")
         os.replace(target + ".tmp", target)
         if verbose:

@@ -289,3 +289,49 @@ def test_api_fast_division_equals_ddiv(monkeypatch):
         assert np.array_equal(a, b)
     assert not K.fast_div_ok(np.array([[1e-320, 1.0, 2.0]]), np.ones((1, 3)))
     assert not K.fast_div_ok(np.ones((1, 3)), np.array([[1e-200, 0.0, 1.0]]))
+
+
+@pytest.mark.parametrize("lambda_th,sigma_dep", [(0.01, 5.0), (0.3, 1.0), (1e-12, 0.0)])
+def test_early_stop_thresholds_against_oracle(mini, lambda_th, sigma_dep):
+    """The warp-level early ray termination at other thresholds than the
+    configs' 1e-4 (the reference's default 0.01, a coarse 0.3 that stops most
+    rays after a few hits, and 1e-12 = never) and depth thresholds (a voxel
+    registers in the depth map above sigma_dep, render.py:40-42)."""
+    sc = dataclasses.replace(mini, lambda_th=lambda_th, sigma_dep=sigma_dep)
+    frame_vs_oracle(sc, KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0], maps64=True)
+
+
+def test_early_stop_alpha_drift_bounded_full_size():
+    """The reference's acceptance property (test_acceptance.py:183-209) at
+    configs[0]'s full size: stopping once alpha exceeds 1 - lambda_th moves
+    every pixel's alpha down by less than lambda_th, never up; a larger
+    threshold never integrates further; depth only loses hits."""
+    from paper_2202_05628_b200.frame import FramePipeline
+
+    sc = S.make_scene("c0")
+    fp = FramePipeline.from_scene(sc)
+    try:
+        pose, cam = KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0]
+        maps = {}
+        for lam in (1e-12, 1e-4, 0.01, 0.3):
+            F, A, D = fp.run(pose, cam, graph=False, maps64=True, lambda_th=lam,
+                             sigma_dep=sc.sigma_dep)
+            fp.stream.synchronize()
+            maps[lam] = (F.cpu().numpy().copy(), A.cpu().numpy().copy(), D.cpu().numpy().copy())
+        A_full = maps[1e-12][1]
+        assert A_full.max() <= 1.0 and (A_full > 0.99).any()
+        prev = A_full
+        for lam in (1e-4, 0.01, 0.3):
+            A = maps[lam][1]
+            drift = A_full - A
+            assert drift.min() >= 0.0 and drift.max() < lam, (lam, drift.min(), drift.max())
+            assert np.all(A <= prev)
+            stopped = A != A_full
+            assert np.all(A[stopped] > 1.0 - lam)
+            # a ray that stopped early keeps every depth hit it had reached
+            D, D_full = maps[lam][2], maps[1e-12][2]
+            assert np.all((D == D_full) | np.isinf(D))
+            prev = A
+        assert (maps[0.3][1] != A_full).any()
+    finally:
+        fp.close()
