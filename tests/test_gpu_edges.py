@@ -291,14 +291,25 @@ def test_api_fast_division_equals_ddiv(monkeypatch):
     assert not K.fast_div_ok(np.ones((1, 3)), np.array([[1e-200, 0.0, 1.0]]))
 
 
+def _opaque(sc, gain=64.0):
+    """The configs' densities (softplus(N(0,1)) over half-voxel steps) leave
+    every pixel's alpha below ~0.35, so no ray ever stops early; scaled by
+    `gain` the body is opaque within a few hits."""
+    fl = sc.flut32.copy()
+    fl[:, -1] *= np.float32(gain)
+    return dataclasses.replace(sc, flut32=fl)
+
+
 @pytest.mark.parametrize("lambda_th,sigma_dep", [(0.01, 5.0), (0.3, 1.0), (1e-12, 0.0)])
 def test_early_stop_thresholds_against_oracle(mini, lambda_th, sigma_dep):
     """The warp-level early ray termination at other thresholds than the
     configs' 1e-4 (the reference's default 0.01, a coarse 0.3 that stops most
     rays after a few hits, and 1e-12 = never) and depth thresholds (a voxel
     registers in the depth map above sigma_dep, render.py:40-42)."""
-    sc = dataclasses.replace(mini, lambda_th=lambda_th, sigma_dep=sigma_dep)
-    frame_vs_oracle(sc, KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0], maps64=True)
+    sc = dataclasses.replace(_opaque(mini), lambda_th=lambda_th, sigma_dep=sigma_dep)
+    want = frame_vs_oracle(sc, KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0], maps64=True)
+    if lambda_th < 1.0e-6:
+        assert (want["A"] > 0.99).any()  # the body is opaque: the other thresholds do stop rays
 
 
 def test_early_stop_alpha_drift_bounded_full_size():
@@ -308,7 +319,7 @@ def test_early_stop_alpha_drift_bounded_full_size():
     threshold never integrates further; depth only loses hits."""
     from paper_2202_05628_b200.frame import FramePipeline
 
-    sc = S.make_scene("c0")
+    sc = _opaque(S.make_scene("c0"))
     fp = FramePipeline.from_scene(sc)
     try:
         pose, cam = KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0]
