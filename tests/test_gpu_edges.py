@@ -312,14 +312,15 @@ def test_early_stop_thresholds_against_oracle(mini, lambda_th, sigma_dep):
         assert (want["A"] > 0.99).any()  # the body is opaque: the other thresholds do stop rays
 
 
-def test_early_stop_alpha_drift_bounded_full_size():
+@pytest.mark.parametrize("config", ["c0", "c2"])
+def test_early_stop_alpha_drift_bounded_full_size(config):
     """The reference's acceptance property (test_acceptance.py:183-209) at
-    configs[0]'s full size: stopping once alpha exceeds 1 - lambda_th moves
+    configs[0]'s and configs[2]'s full size: stopping once alpha exceeds 1 - lambda_th moves
     every pixel's alpha down by less than lambda_th, never up; a larger
     threshold never integrates further; depth only loses hits."""
     from paper_2202_05628_b200.frame import FramePipeline
 
-    sc = _opaque(S.make_scene("c0"))
+    sc = _opaque(S.make_scene(config))
     fp = FramePipeline.from_scene(sc)
     try:
         pose, cam = KM.PoseSpec.make(sc.poses[0]), sc.cameras[0][0]
